@@ -1,0 +1,202 @@
+/*
+ * undertext_b200.h -- C ABI of the B200-native CVA / PCA hot path.
+ *
+ * Drop-in boundary for the reference package `undertext`
+ * (/root/reference/pkg/src/undertext).  The reference is pure Python + numpy;
+ * its "plugin interface" for this path is the set of Python functions listed
+ * next to each entry point below.  A maintainer binds these symbols with
+ * ctypes; the in-tree Python mirror
+ * (paper_1612_06457_b200/) does exactly that.
+ *
+ * Conventions:
+ *   - every function returns a status: UT_OK, UT_EDATA (-> DataError),
+ *     UT_ENUMERIC (-> NumericError), UT_ECUDA (-> RuntimeError); no C++
+ *     exception crosses the ABI; ut_last_error() gives the message (per thread);
+ *   - all array pointers are DEVICE pointers owned by the caller unless the
+ *     parameter is documented as host; the library never frees them;
+ *   - every call takes the caller's stream (a cudaStream_t passed as void*),
+ *     enqueues asynchronously and never synchronizes, so calls are capturable
+ *     in CUDA graphs; the device is the one current on the calling thread;
+ *   - data-dependent failures (bad point, non-PD matrix) are reported through
+ *     small device-side status words the caller reads when it needs them.
+ *   - matrices are row-major: m[i*ld + j].
+ */
+#ifndef UNDERTEXT_B200_H
+#define UNDERTEXT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UT_OK 0
+#define UT_EDATA 1
+#define UT_ENUMERIC 2
+#define UT_ECUDA 3
+
+/* sample types of a spectral cube (SpectralStack.planes dtype, stack.py:43-49) */
+enum { UT_U8 = 0, UT_U16 = 1, UT_F16 = 2, UT_F32 = 3, UT_F64 = 4 };
+
+/* device-side info codes written by the solvers */
+enum {
+  UT_INFO_OK = 0,
+  UT_INFO_ASYM_A = 1,      /* eigen.py:90  _check_symmetric(A) */
+  UT_INFO_ASYM_M = 2,      /* eigen.py:91  _check_symmetric(M) */
+  UT_INFO_NOT_PD = 3,      /* eigen.py:94-104 cholesky failed (aux = eig(M')) */
+  UT_INFO_NO_CONVERGE = 4  /* Jacobi sweep cap reached (never seen in tests) */
+};
+
+/* A band-sequential cube (or a row shard of one), SpectralStack.planes (B,H,W). */
+typedef struct {
+  const void* data;      /* device pointer to element (band 0, local row 0, col 0) */
+  int32_t dtype;         /* UT_U8 .. UT_F64 */
+  int32_t bands;         /* B, 1..32 */
+  int64_t rows;          /* local rows */
+  int64_t cols;          /* W */
+  int64_t band_stride;   /* elements between bands */
+  int64_t row_stride;    /* elements between rows */
+  int64_t row0;          /* global row index of local row 0 (row sharding) */
+} ut_cube;
+
+/* Outputs of ut_cva_solve (all device pointers, B = bands, C = classes). */
+typedef struct {
+  double* within;        /* B*B  ScatterPair.within   (projection.py:199) */
+  double* between;       /* B*B  ScatterPair.between  (projection.py:200) */
+  double* class_means;   /* C*B  ScatterPair.class_means */
+  double* counts;        /* C    ScatterPair.counts (exact integers) */
+  double* grand_mean;    /* B    ScatterPair.grand_mean = ProjectionModel.mean */
+  double* evals;         /* B    descending (eigen.py:111) */
+  double* evecs;         /* B*B  column j = eigenvector j, M'-orthonormal, sign-normalized */
+  double* aux;           /* B    eig(M') when info == UT_INFO_NOT_PD */
+  int32_t* info;         /* 1 */
+} ut_cva_out;
+
+/* Outputs of ut_pca_solve (projection.py:335-338 + _pca_from_covariance :263-270). */
+typedef struct {
+  double* mean;          /* B */
+  double* std;           /* B  (0 -> 1 as projection.py:336) */
+  double* corr;          /* B*B correlation matrix that is diagonalized */
+  double* evals;         /* B descending */
+  double* evecs;         /* B*B orthonormal, sign-normalized */
+  int32_t* info;         /* 1 */
+} ut_pca_out;
+
+/* ---------------------------------------------------------------- misc */
+int ut_version(void);
+const char* ut_last_error(void);
+/* number of doubles in one class-moment record: 1 + B + B*B */
+int64_t ut_moment_len(int32_t bands);
+
+/* ------------------------------------------------- K1: training gather
+ * Replaces annotations.assemble_matrix's point loop (annotations.py:195-215):
+ * values[b*ld + j] = (double) cube[b, y_j - row0, x_j] for the n points
+ * xy = [x0,y0,x1,y1,...] (global coordinates).  first_bad receives the lowest
+ * index of an out-of-bounds point, or -1 (DataError in the reference,
+ * annotations.py:208-212). */
+int ut_gather(const ut_cube* cube, const int32_t* xy, int64_t n,
+              double* values, int64_t ld, int64_t* first_bad, void* stream);
+
+/* ------------------------------------------------- K1: class moments
+ * Per-class count, mean and centred scatter M2 of a B x n design matrix
+ * (two-pass, like compute_scatter's per-class loop, projection.py:187-198).
+ * cls[j] in [0, classes) is the class *index* of point j (index into the sorted
+ * unique labels).  moments: classes records of ut_moment_len(B) doubles:
+ * [count, mean(B), M2(B*B)].  ws: ut_class_moments_ws(n, B, C) bytes. */
+size_t ut_class_moments_ws(int64_t n, int32_t bands, int32_t classes);
+int ut_class_moments(const double* values, int64_t ld, const int32_t* cls,
+                     int64_t n, int32_t bands, int32_t classes, double* moments,
+                     void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------- K3: CVA solve
+ * Combines `groups` partial moment sets (rank-major [groups][classes][len],
+ * e.g. all-gathered from row shards) with the parallel-axis rule, builds the
+ * symmetrized within / between scatter (projection.py:190-200), then solves
+ * between v = lambda (within + ridge*tr/B*I) v in one CTA (eigen.py:63-113). */
+int ut_cva_solve(const double* moments, int32_t groups, int32_t bands,
+                 int32_t classes, double ridge, const ut_cva_out* out, void* stream);
+
+/* ------------------------------------------------- K3: eigensolver
+ * solve_gen_eig_sym(A, M, ridge) (eigen.py:75-113).  M == NULL selects the
+ * plain symmetric problem with no ridge and orthonormal vectors (the
+ * np.linalg.eigh + sign_normalize of _pca_from_covariance, projection.py:263). */
+int ut_gen_eig_sym(const double* A, const double* M, int32_t bands, double ridge,
+                   double* evals, double* evecs, double* aux, int32_t* info,
+                   void* stream);
+
+/* ------------------------------------------------- K2: region moments
+ * One pass over a region (x0, y0, w, h) in *local* row coordinates:
+ * moments = [n, mean(B), M2(B*B)] (projection.py:325-334, shifted one-pass
+ * form; shift = mean of a fixed strided sample).  ws: ut_region_moments_ws. */
+size_t ut_region_moments_ws(int32_t bands);
+int ut_region_moments(const ut_cube* cube, int64_t x0, int64_t y0, int64_t w,
+                      int64_t h, double* moments, void* ws, size_t ws_bytes,
+                      void* stream);
+
+/* ------------------------------------------------- K3: PCA solve
+ * Combines `groups` region-moment records, then std / correlation /
+ * eigh / top-k / sign-normalize (projection.py:335-338, :263-270). */
+int ut_pca_solve(const double* moments, int32_t groups, int32_t bands,
+                 const ut_pca_out* out, void* stream);
+
+/* ------------------------------------------------- K4: projector
+ * project_stack / _project_rows (projection.py:371-439) fused with the global
+ * min/max of rescale_full (rendering.py:126-127).
+ * coef: B x ld_coef row-major (ProjectionModel.coefficients, or evecs);
+ * components (HOST array of k indices into coef columns); mean (B); std (B or
+ * NULL for methods without standardization).  scores: k planes of rows*cols
+ * float32, dense.  minmax: 2k floats [-min_0..-min_{k-1}, max_0..max_{k-1}]
+ * (negated mins so a MAX all-reduce combines shards).  nonfinite: 1 int set
+ * non-zero if any score is NaN/Inf (ScorePlane check, rendering.py:49-50).
+ * precision: 0 = fp32 FMA on centred samples with an fp64-exact mean split,
+ *            1 = fp64 throughout.  ws: ut_project_ws(). */
+size_t ut_project_ws(void);
+int ut_project_minmax(const ut_cube* cube, const double* coef, int32_t ld_coef,
+                      const int32_t* components, int32_t k, const double* mean,
+                      const double* std, int32_t precision, float* scores,
+                      float* minmax, int32_t* nonfinite, void* ws, size_t ws_bytes,
+                      void* stream);
+
+/* ------------------------------------------------- K5: stretch
+ * rescale_full -> linear_to_codes -> round_half_away (rendering.py:124-130,
+ * quantize.py:13-46) for k dense planes of npix float32 scores, using the
+ * minmax record produced by ut_project_minmax (possibly all-reduced):
+ * plane c uses lo = -minmax[c], hi = minmax[ld_minmax + c].
+ * depth 8 -> uint8 codes, 16 -> uint16.  lo == hi renders zeros. */
+int ut_stretch(const float* scores, const float* minmax, int32_t k, int32_t ld_minmax,
+               int64_t npix, int32_t depth, void* codes, void* stream);
+
+/* ------------------------------------------------- single planes
+ * rescale_full on an arbitrary float32/float64 plane (e.g. a host ScorePlane):
+ * lohi[0] = min, lohi[1] = max (rendering.py:126-127); nonfinite set if a
+ * NaN/Inf is present (ScorePlane check, rendering.py:49-50). */
+size_t ut_plane_minmax_ws(void);
+int ut_plane_minmax(const void* plane, int32_t dtype, int64_t n, double* lohi,
+                    int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream);
+/* linear_to_codes(values, lo, hi, depth) (quantize.py:36-46) with device
+ * lohi = {lo, hi}; lo == hi (constant plane) gives zeros. */
+int ut_linear_to_codes(const void* plane, int32_t dtype, int64_t n, const double* lohi,
+                       int32_t depth, void* codes, void* stream);
+
+/* ------------------------------------------------- synthetic cubes
+ * Seeded generator for the BASELINE.json configs: class map
+ * from `nshapes` shapes (rects kind 0: [y0,x0,y1,x1); ellipses kind 1:
+ * [cy,cx,ry,rx]) evaluated in integer arithmetic, later shapes win; pixel =
+ * means[c] + chol[c] z (z ~ N(0,1) from a counter hash of seed/pixel/band),
+ * clipped to [0,1] and cast (u16: round_half_away(4095 v)).
+ * means: C*B doubles, chol: C*B*B doubles (row-major lower), shapes: HOST
+ * int64 [nshapes][6] = {kind, class, a, b, c, d}.  Rows [row0, row0+rows). */
+int ut_synth_cube(const ut_cube* cube, int64_t height, const double* means,
+                  const double* chol, int32_t classes, const int64_t* shapes,
+                  int32_t nshapes, uint64_t seed, void* stream);
+
+/* class index of pixels (x_j, y_j): for host-side training-point sampling
+ * checks (device version of the same integer class map). */
+int ut_class_of(const int64_t* shapes, int32_t nshapes, const int32_t* xy,
+                int64_t n, int32_t* cls, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UNDERTEXT_B200_H */

@@ -1,0 +1,106 @@
+"""ctypes binding of the C ABI in include/undertext_b200.h.
+
+This is the one place Python touches the native library.  There is no
+fallback: if ``lib/libundertext_b200.so`` is missing or fails to load, every
+compute entry point raises ``RuntimeError`` (run ``__graft_entry__.build()`` or
+``python -m paper_1612_06457_b200.build``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+from .errors import DataError, NumericError
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libundertext_b200.so"
+
+UT_OK, UT_EDATA, UT_ENUMERIC, UT_ECUDA = 0, 1, 2, 3
+UT_U8, UT_U16, UT_F16, UT_F32, UT_F64 = 0, 1, 2, 3, 4
+INFO_OK, INFO_ASYM_A, INFO_ASYM_M, INFO_NOT_PD, INFO_NO_CONVERGE = 0, 1, 2, 3, 4
+
+# every symbol include/undertext_b200.h declares (checked by the CPU tests)
+EXPORTS = (
+    "ut_version", "ut_last_error", "ut_moment_len", "ut_gather", "ut_class_moments_ws",
+    "ut_class_moments", "ut_cva_solve", "ut_gen_eig_sym", "ut_region_moments_ws",
+    "ut_region_moments", "ut_pca_solve", "ut_project_ws", "ut_project_minmax",
+    "ut_stretch", "ut_plane_minmax_ws", "ut_plane_minmax", "ut_linear_to_codes",
+    "ut_synth_cube", "ut_class_of",
+)
+
+
+class Cube(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("dtype", C.c_int32), ("bands", C.c_int32),
+                ("rows", C.c_int64), ("cols", C.c_int64), ("band_stride", C.c_int64),
+                ("row_stride", C.c_int64), ("row0", C.c_int64)]
+
+
+class CvaOut(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("within", "between", "class_means", "counts",
+                                           "grand_mean", "evals", "evecs", "aux", "info")]
+
+
+class PcaOut(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("mean", "std", "corr", "evals", "evecs", "info")]
+
+
+_lock = threading.Lock()
+_lib = None
+
+P = C.c_void_p
+I32, I64, SZ, F64 = C.c_int32, C.c_int64, C.c_size_t, C.c_double
+
+_SIGS = {
+    "ut_version": (I32, []),
+    "ut_last_error": (C.c_char_p, []),
+    "ut_moment_len": (I64, [I32]),
+    "ut_gather": (I32, [C.POINTER(Cube), P, I64, P, I64, P, P]),
+    "ut_class_moments_ws": (SZ, [I64, I32, I32]),
+    "ut_class_moments": (I32, [P, I64, P, I64, I32, I32, P, P, SZ, P]),
+    "ut_cva_solve": (I32, [P, I32, I32, I32, F64, C.POINTER(CvaOut), P]),
+    "ut_gen_eig_sym": (I32, [P, P, I32, F64, P, P, P, P, P]),
+    "ut_region_moments_ws": (SZ, [I32]),
+    "ut_region_moments": (I32, [C.POINTER(Cube), I64, I64, I64, I64, P, P, SZ, P]),
+    "ut_pca_solve": (I32, [P, I32, I32, C.POINTER(PcaOut), P]),
+    "ut_project_ws": (SZ, []),
+    "ut_project_minmax": (I32, [C.POINTER(Cube), P, I32, P, I32, P, P, I32, P, P, P, P, SZ, P]),
+    "ut_stretch": (I32, [P, P, I32, I32, I64, I32, P, P]),
+    "ut_plane_minmax_ws": (SZ, []),
+    "ut_plane_minmax": (I32, [P, I32, I64, P, P, P, SZ, P]),
+    "ut_linear_to_codes": (I32, [P, I32, I64, P, I32, P, P]),
+    "ut_synth_cube": (I32, [C.POINTER(Cube), I64, P, P, I32, P, I32, C.c_uint64, P]),
+    "ut_class_of": (I32, [P, I32, P, I64, P, P]),
+}
+
+
+def lib():
+    """Load (once) and return the native library; raise loudly if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RuntimeError(
+                    f"B200 library not built: {LIB_PATH} is missing "
+                    "(run __graft_entry__.build()); there is no CPU fallback")
+            handle = C.CDLL(str(LIB_PATH))
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    """Map a C-ABI status onto the reference's exception contract."""
+    if rc == UT_OK:
+        return
+    msg = lib().ut_last_error().decode(errors="replace") or what
+    if rc == UT_EDATA:
+        raise DataError(msg)
+    if rc == UT_ENUMERIC:
+        raise NumericError(msg)
+    raise RuntimeError(msg)

@@ -1,0 +1,108 @@
+// Shared helpers for the sm_100a kernels of the CVA / PCA hot path.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cfloat>
+#include <type_traits>
+#include <cstdio>
+
+#include "../../include/undertext_b200.h"
+
+namespace ut {
+
+constexpr int kMaxBands = 32;
+
+// ---------------------------------------------------------------- errors
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* where);
+
+#define UT_CHECK_LAUNCH(where)                                   \
+  do {                                                           \
+    cudaError_t _e = cudaGetLastError();                         \
+    if (_e != cudaSuccess) return ::ut::cuda_status(_e, where);  \
+  } while (0)
+
+#define UT_REQUIRE(cond, ...)         \
+  do {                                \
+    if (!(cond)) {                    \
+      ::ut::set_error(__VA_ARGS__);   \
+      return UT_EDATA;                \
+    }                                 \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count();
+
+// ---------------------------------------------------------------- samples
+template <typename T> struct Sample;
+template <> struct Sample<uint8_t>  { static constexpr int code = UT_U8; };
+template <> struct Sample<uint16_t> { static constexpr int code = UT_U16; };
+template <> struct Sample<__half>   { static constexpr int code = UT_F16; };
+template <> struct Sample<float>    { static constexpr int code = UT_F32; };
+template <> struct Sample<double>   { static constexpr int code = UT_F64; };
+
+__device__ __forceinline__ float to_f32(uint8_t v) { return (float)v; }
+__device__ __forceinline__ float to_f32(uint16_t v) { return (float)v; }
+__device__ __forceinline__ float to_f32(__half v) { return __half2float(v); }
+__device__ __forceinline__ float to_f32(float v) { return v; }
+__device__ __forceinline__ float to_f32(double v) { return (float)v; }
+
+__device__ __forceinline__ double to_f64(uint8_t v) { return (double)v; }
+__device__ __forceinline__ double to_f64(uint16_t v) { return (double)v; }
+__device__ __forceinline__ double to_f64(__half v) { return (double)__half2float(v); }
+__device__ __forceinline__ double to_f64(float v) { return (double)v; }
+__device__ __forceinline__ double to_f64(double v) { return v; }
+
+// Streaming 128-bit global loads: read once, do not pollute L1.
+__device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream_u4(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// Unpack a 16-byte vector into V = 16/sizeof(T) samples.
+template <typename T> struct Vec {
+  static constexpr int V = 16 / sizeof(T);
+  __device__ __forceinline__ static void unpack_f32(const uint4& u, float* out) {
+    const T* t = reinterpret_cast<const T*>(&u);
+#pragma unroll
+    for (int i = 0; i < V; ++i) out[i] = to_f32(t[i]);
+  }
+  __device__ __forceinline__ static void unpack_f64(const uint4& u, double* out) {
+    const T* t = reinterpret_cast<const T*>(&u);
+#pragma unroll
+    for (int i = 0; i < V; ++i) out[i] = to_f64(t[i]);
+  }
+};
+
+// Order-preserving float <-> uint encoding (for atomics-free min/max merges).
+__device__ __forceinline__ float nan_guard(float acc, float v) { return fmaf(0.0f, v, acc); }
+
+// Block-wide "last CTA finishes" ticket: returns true in exactly one CTA, after
+// every CTA's preceding global writes are visible.  *counter must be 0 on entry
+// of the launch; the last CTA resets it.
+__device__ __forceinline__ bool last_block_ticket(unsigned int* counter) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int t = atomicAdd(counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+}  // namespace ut

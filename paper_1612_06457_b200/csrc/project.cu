@@ -1,0 +1,487 @@
+// K4 + K5: per-pixel projection fused with the global min/max, and the
+// full-range uint8/uint16 stretch.
+//
+// Reference: project_stack / _project_rows (projection.py:371-439),
+// rescale_full (rendering.py:124-130), linear_to_codes / round_half_away
+// (quantize.py:13-46).
+//
+// K4 streams the band-sequential cube once (HBM-bound: B*s bytes per pixel),
+// each thread owning VEC adjacent pixels and issuing one 4/8/16-byte
+// L1-bypassing load per band, eight bands in flight.  Per pixel it forms
+// score_k = sum_b w_bk (x_b - m_b) in fixed band order, writes the fp32 score
+// planes with streaming stores, and keeps a running min/max per component; the
+// CTA partials are merged in fixed order by the last CTA to finish, so the
+// result is deterministic and needs no init kernel.  The min is stored negated
+// ([-min.., max..]) so a MAX all-reduce merges row shards.
+//
+// K5 re-reads the fp32 planes and applies the reference's arithmetic exactly
+// in fp64: code = floor(clip((v - lo) * (top / (hi - lo)), 0, top) + 0.5).
+#include "common.cuh"
+
+namespace ut {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxGroup = 8;      // components per pass over the cube
+constexpr int kMaxGroups = 4;     // 4 * 8 = 32 >= B >= K
+constexpr int kMaxGrid = 4096;
+constexpr int kBandUnroll = 8;
+
+struct ProjParams {
+  const void* data;
+  int64_t bs, rs, rows, cols, npix;
+  int bands;
+  int k0, ktotal;          // this pass covers components [k0, k0 + KG) of ktotal
+  int comps[kMaxGroup];    // column of coef for each component of this pass
+  const double* coef;
+  int ld_coef;
+  const double* mean;
+  const double* std;       // nullable
+  float* scores;           // plane (k0 + k) at scores + (k0 + k) * npix
+  float* minmax;           // 2 * ktotal
+  int* nonfinite;
+  float* part;             // [grid][2 * KG]
+  unsigned int* counter;
+};
+
+template <int BYTES> struct Ld;
+template <> struct Ld<16> {
+  using U = uint4;
+  __device__ __forceinline__ static U load(const void* p) { return ld_stream_u4(p); }
+};
+template <> struct Ld<8> {
+  using U = uint2;
+  __device__ __forceinline__ static U load(const void* p) {
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                 : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+  }
+};
+template <> struct Ld<4> {
+  using U = uint32_t;
+  __device__ __forceinline__ static U load(const void* p) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+  }
+};
+
+// Centred sample in the accumulation type.  In the fp32 path the mean is split
+// as hi + lo (hi = fp32(mean)); the lo part is folded into a per-component
+// fp64-computed bias so the centring error is only the rounding of x - hi.
+template <typename T> __device__ __forceinline__ float centred_f32(T x, float hi, double mean) {
+  return to_f32(x) - hi;
+}
+template <> __device__ __forceinline__ float centred_f32<double>(double x, float, double mean) {
+  return (float)(x - mean);
+}
+
+// Scores are always stored as fp32.
+template <int VEC> __device__ __forceinline__ void store_scores(float* dst, const float* v) {
+  if constexpr (VEC == 4) {
+    st_stream_u4(dst, make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]),
+                                 __float_as_uint(v[2]), __float_as_uint(v[3])));
+  } else if constexpr (VEC == 8) {
+    st_stream_u4(dst, make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]),
+                                 __float_as_uint(v[2]), __float_as_uint(v[3])));
+    st_stream_u4(dst + 4, make_uint4(__float_as_uint(v[4]), __float_as_uint(v[5]),
+                                     __float_as_uint(v[6]), __float_as_uint(v[7])));
+  } else if constexpr (VEC == 16) {
+#pragma unroll
+    for (int i = 0; i < 16; i += 4)
+      st_stream_u4(dst + i, make_uint4(__float_as_uint(v[i]), __float_as_uint(v[i + 1]),
+                                       __float_as_uint(v[i + 2]), __float_as_uint(v[i + 3])));
+  } else if constexpr (VEC == 2) {
+    asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(dst), "f"(v[0]), "f"(v[1]) : "memory");
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) dst[i] = v[i];
+  }
+}
+
+template <typename T, int VEC, int KG, bool F64>
+struct Proj {
+  using Acc = typename std::conditional<F64, double, float>::type;
+  static constexpr int LB = VEC * (int)sizeof(T);  // load bytes per band
+
+  // shared: weights [B][KG], shifts [B], bias [KG]
+  struct Smem {
+    Acc w[kMaxBands][KG];
+    float hi[kMaxBands];
+    double mean[kMaxBands];
+    Acc bias[KG];
+    float red[kThreads / 32][2 * KG + 1];
+  };
+
+  __device__ static void setup(const ProjParams& p, Smem& s) {
+    for (int e = threadIdx.x; e < p.bands * KG; e += blockDim.x) {
+      const int b = e / KG, k = e - b * KG;
+      double w = p.coef[(int64_t)b * p.ld_coef + p.comps[k]];
+      if (p.std) w = w / p.std[b];
+      s.w[b][k] = (Acc)w;
+    }
+    for (int b = threadIdx.x; b < p.bands; b += blockDim.x) {
+      s.mean[b] = p.mean[b];
+      s.hi[b] = (float)p.mean[b];
+    }
+    __syncthreads();
+    if (threadIdx.x < KG) {
+      const int k = threadIdx.x;
+      double bias = 0.0;
+      if (!F64 && !std::is_same<T, double>::value) {
+        // bias = -sum_b w_f (mean_b - hi_b): exact hi/lo split of the mean
+        // (fp64 samples are centred on the full mean in fp64 instead)
+        for (int b = 0; b < p.bands; ++b)
+          bias -= (double)s.w[b][k] * (s.mean[b] - (double)s.hi[b]);
+      }
+      s.bias[k] = (Acc)bias;
+    }
+    __syncthreads();
+  }
+
+  // One VEC-pixel group starting at pixel index `base` (vectorized, contiguous planes).
+  __device__ static void group_vec(const ProjParams& p, const Smem& s, int64_t base, float* mn,
+                                   float* mx, float& chk) {
+    const char* src = static_cast<const char*>(p.data) + base * (int64_t)sizeof(T);
+    const int64_t bstride = p.bs * (int64_t)sizeof(T);
+    Acc acc[KG][VEC];
+#pragma unroll
+    for (int k = 0; k < KG; ++k)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[k][v] = s.bias[k];
+    for (int b0 = 0; b0 < p.bands; b0 += kBandUnroll) {
+      typename Ld<LB>::U raw[kBandUnroll];
+#pragma unroll
+      for (int u = 0; u < kBandUnroll; ++u)
+        if (b0 + u < p.bands) raw[u] = Ld<LB>::load(src + (int64_t)(b0 + u) * bstride);
+#pragma unroll
+      for (int u = 0; u < kBandUnroll; ++u) {
+        const int b = b0 + u;
+        if (b < p.bands) {
+          const T* xs = reinterpret_cast<const T*>(&raw[u]);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            Acc d;
+            if constexpr (F64) d = to_f64(xs[v]) - s.mean[b];
+            else d = centred_f32<T>(xs[v], s.hi[b], s.mean[b]);
+#pragma unroll
+            for (int k = 0; k < KG; ++k) acc[k][v] = fma(s.w[b][k], d, acc[k][v]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      float out[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        out[v] = (float)acc[k][v];
+        mn[k] = fminf(mn[k], out[v]);
+        mx[k] = fmaxf(mx[k], out[v]);
+        chk = nan_guard(chk, out[v]);
+      }
+      store_scores<VEC>(p.scores + (int64_t)(p.k0 + k) * p.npix + base, out);
+    }
+  }
+
+  // One pixel with general strides (tails, views, misaligned inputs).
+  __device__ static void pixel_any(const ProjParams& p, const Smem& s, int64_t pix, float* mn,
+                                   float* mx, float& chk) {
+    const int64_t row = pix / p.cols, col = pix - row * p.cols;
+    const T* src = static_cast<const T*>(p.data) + row * p.rs + col;
+    Acc acc[KG];
+#pragma unroll
+    for (int k = 0; k < KG; ++k) acc[k] = s.bias[k];
+    for (int b = 0; b < p.bands; ++b) {
+      const T x = src[(int64_t)b * p.bs];
+      Acc d;
+      if constexpr (F64) d = to_f64(x) - s.mean[b];
+      else d = centred_f32<T>(x, s.hi[b], s.mean[b]);
+#pragma unroll
+      for (int k = 0; k < KG; ++k) acc[k] = fma(s.w[b][k], d, acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      const float o = (float)acc[k];
+      mn[k] = fminf(mn[k], o);
+      mx[k] = fmaxf(mx[k], o);
+      chk = nan_guard(chk, o);
+      p.scores[(int64_t)(p.k0 + k) * p.npix + pix] = o;
+    }
+  }
+
+  __device__ static void finish(const ProjParams& p, Smem& s, float* mn, float* mx, float chk) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      for (int o = 16; o > 0; o >>= 1) {
+        mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
+        mx[k] = fmaxf(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) chk += __shfl_xor_sync(0xffffffffu, chk, o);
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        s.red[warp][k] = -mn[k];
+        s.red[warp][KG + k] = mx[k];
+      }
+      s.red[warp][2 * KG] = chk;
+    }
+    __syncthreads();
+    if (threadIdx.x <= 2 * KG) {
+      const int f = threadIdx.x;
+      float r = s.red[0][f];
+      for (int w = 1; w < kThreads / 32; ++w)
+        r = (f == 2 * KG) ? r + s.red[w][f] : fmaxf(r, s.red[w][f]);
+      p.part[(int64_t)blockIdx.x * (2 * KG + 1) + f] = r;
+    }
+    if (last_block_ticket(p.counter)) {
+      if (threadIdx.x <= 2 * KG) {
+        const int f = threadIdx.x;
+        float r = p.part[f];
+        for (unsigned int g = 1; g < gridDim.x; ++g) {
+          const float o = p.part[(int64_t)g * (2 * KG + 1) + f];
+          r = (f == 2 * KG) ? r + o : fmaxf(r, o);
+        }
+        if (f == 2 * KG) {
+          if (r != 0.0f) atomicOr(p.nonfinite, 1);  // NaN or Inf seen
+        } else if (f < KG) {
+          p.minmax[p.k0 + f] = r;
+        } else {
+          p.minmax[p.ktotal + p.k0 + (f - KG)] = r;
+        }
+      }
+      if (threadIdx.x == 0) *p.counter = 0u;
+    }
+  }
+};
+
+template <typename T, int VEC, int KG, bool F64, bool VECTOR>
+__global__ void __launch_bounds__(kThreads)
+project_kernel(ProjParams p) {
+  using P = Proj<T, VEC, KG, F64>;
+  __shared__ typename P::Smem s;
+  P::setup(p, s);
+  float mn[KG], mx[KG], chk = 0.0f;
+#pragma unroll
+  for (int k = 0; k < KG; ++k) {
+    mn[k] = INFINITY;
+    mx[k] = -INFINITY;
+  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if constexpr (VECTOR) {
+    const int64_t groups = p.npix / VEC;
+    for (int64_t g = tid; g < groups; g += stride) P::group_vec(p, s, g * VEC, mn, mx, chk);
+    for (int64_t pix = groups * VEC + tid; pix < p.npix; pix += stride)
+      P::pixel_any(p, s, pix, mn, mx, chk);
+  } else {
+    for (int64_t pix = tid; pix < p.npix; pix += stride) P::pixel_any(p, s, pix, mn, mx, chk);
+  }
+  P::finish(p, s, mn, mx, chk);
+}
+
+template <typename T, int VEC, int KG, bool F64, bool VECTOR>
+int launch_one(ProjParams& p, cudaStream_t st) {
+  auto kern = project_kernel<T, VEC, KG, F64, VECTOR>;
+  static int per_sm = 0;  // resident CTAs per SM for this instantiation
+  if (per_sm == 0) {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, 0);
+    per_sm = n > 0 ? n : 1;
+  }
+  const int64_t units = VECTOR ? (p.npix + VEC - 1) / VEC : p.npix;
+  int64_t grid = (int64_t)per_sm * sm_count();
+  const int64_t need = (units + kThreads - 1) / kThreads;
+  if (grid > need) grid = need;
+  if (grid > kMaxGrid) grid = kMaxGrid;
+  if (grid < 1) grid = 1;
+  kern<<<(int)grid, kThreads, 0, st>>>(p);
+  UT_CHECK_LAUNCH("project_kernel");
+  return UT_OK;
+}
+
+template <typename T, int KG, bool F64>
+int launch_kg(ProjParams& p, bool vector_ok, cudaStream_t st) {
+  // pixels per thread: one 16-byte load per band, capped so KG*VEC <= 32 accumulators
+  constexpr int V16 = 16 / (int)sizeof(T);
+  constexpr int VCAP = (32 / KG) >= 16 ? 16 : (32 / KG) >= 8 ? 8 : (32 / KG) >= 4 ? 4 : 2;
+  constexpr int VEC = V16 < VCAP ? V16 : VCAP;
+  constexpr int LB = VEC * (int)sizeof(T);
+  const bool aligned = vector_ok &&
+                       (reinterpret_cast<uintptr_t>(p.data) % LB == 0) &&
+                       ((p.bs * (int64_t)sizeof(T)) % LB == 0) &&
+                       (reinterpret_cast<uintptr_t>(p.scores) % 16 == 0) &&
+                       (p.npix % 4 == 0);
+  if (aligned) return launch_one<T, VEC, KG, F64, true>(p, st);
+  return launch_one<T, 1, KG, F64, false>(p, st);
+}
+
+template <typename T, bool F64>
+int launch_t(ProjParams& p, int kg, bool vector_ok, cudaStream_t st) {
+  switch (kg) {
+    case 1: return launch_kg<T, 1, F64>(p, vector_ok, st);
+    case 2: return launch_kg<T, 2, F64>(p, vector_ok, st);
+    case 3: return launch_kg<T, 3, F64>(p, vector_ok, st);
+    case 4: return launch_kg<T, 4, F64>(p, vector_ok, st);
+    case 5: return launch_kg<T, 5, F64>(p, vector_ok, st);
+    case 6: return launch_kg<T, 6, F64>(p, vector_ok, st);
+    case 7: return launch_kg<T, 7, F64>(p, vector_ok, st);
+    case 8: return launch_kg<T, 8, F64>(p, vector_ok, st);
+  }
+  set_error("project: bad component group %d", kg);
+  return UT_EDATA;
+}
+
+template <bool F64>
+int launch_prec(ProjParams& p, int dtype, int kg, bool vector_ok, cudaStream_t st) {
+  switch (dtype) {
+    case UT_U8: return launch_t<uint8_t, F64>(p, kg, vector_ok, st);
+    case UT_U16: return launch_t<uint16_t, F64>(p, kg, vector_ok, st);
+    case UT_F16: return launch_t<__half, F64>(p, kg, vector_ok, st);
+    case UT_F32: return launch_t<float, F64>(p, kg, vector_ok, st);
+    case UT_F64: return launch_t<double, F64>(p, kg, vector_ok, st);
+  }
+  set_error("project: unknown dtype %d", dtype);
+  return UT_EDATA;
+}
+
+// ------------------------------------------------------------------ K5
+template <int DEPTH>
+__global__ void __launch_bounds__(kThreads)
+stretch_kernel(const float* __restrict__ scores, const float* __restrict__ minmax, int k,
+               int ld_mm, int64_t npix, void* __restrict__ codes_raw, bool vec16) {
+  using Code = typename std::conditional<DEPTH == 8, uint8_t, uint16_t>::type;
+  constexpr double top = DEPTH == 8 ? 255.0 : 65535.0;
+  __shared__ double lo_s[kMaxBands], sc_s[kMaxBands];
+  __shared__ int flat_s[kMaxBands];
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    const double lo = -(double)minmax[c], hi = (double)minmax[ld_mm + c];
+    lo_s[c] = lo;
+    flat_s[c] = (lo == hi) || !(lo < hi);  // constant plane (rendering.py:128-129)
+    sc_s[c] = flat_s[c] ? 0.0 : top / (hi - lo);
+  }
+  __syncthreads();
+  Code* codes = static_cast<Code*>(codes_raw);
+  const int64_t total = (int64_t)k * npix;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  auto code_of = [&](float v, int c) -> Code {
+    if (flat_s[c]) return (Code)0;
+    double x = ((double)v - lo_s[c]) * sc_s[c];
+    x = fmin(fmax(x, 0.0), top);
+    return (Code)(int)floor(x + 0.5);
+  };
+  if (vec16) {
+    // 16 consecutive scores of one plane per thread (npix % 16 == 0)
+    const int64_t chunks = total / 16;
+    for (int64_t q = tid; q < chunks; q += stride) {
+      const int64_t e0 = q * 16;
+      const int c = (int)(e0 / npix);
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; i += 4) {
+        const uint4 u = ld_stream_u4(scores + e0 + i);
+        v[i] = __uint_as_float(u.x);
+        v[i + 1] = __uint_as_float(u.y);
+        v[i + 2] = __uint_as_float(u.z);
+        v[i + 3] = __uint_as_float(u.w);
+      }
+      Code out[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) out[i] = code_of(v[i], c);
+      if constexpr (DEPTH == 8) {
+        st_stream_u4(codes + e0, *reinterpret_cast<const uint4*>(out));
+      } else {
+        st_stream_u4(codes + e0, *reinterpret_cast<const uint4*>(out));
+        st_stream_u4(codes + e0 + 8, *reinterpret_cast<const uint4*>(out + 8));
+      }
+    }
+  } else {
+    for (int64_t e = tid; e < total; e += stride) codes[e] = code_of(scores[e], (int)(e / npix));
+  }
+}
+
+}  // namespace
+}  // namespace ut
+
+using namespace ut;
+
+extern "C" {
+
+size_t ut_project_ws(void) {
+  return 256 + sizeof(float) * (size_t)kMaxGroups * kMaxGrid * (2 * kMaxGroup + 1);
+}
+
+int ut_project_minmax(const ut_cube* cube, const double* coef, int32_t ld_coef,
+                      const int32_t* components, int32_t k, const double* mean,
+                      const double* std, int32_t precision, float* scores, float* minmax,
+                      int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream) {
+  UT_REQUIRE(cube && cube->bands >= 1 && cube->bands <= kMaxBands,
+             "ut_project_minmax: bands must be 1..32");
+  UT_REQUIRE(k >= 1 && k <= kMaxGroup * kMaxGroups, "ut_project_minmax: k must be 1..32");
+  UT_REQUIRE(ws_bytes >= ut_project_ws(), "ut_project_minmax: workspace too small");
+  UT_REQUIRE(cube->rows >= 1 && cube->cols >= 1, "ut_project_minmax: empty cube");
+  for (int i = 0; i < k; ++i)
+    UT_REQUIRE(components[i] >= 0 && components[i] < ld_coef,
+               "component %d out of range", components[i]);
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaMemsetAsync(ws, 0, 256, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), st);
+  if (e != cudaSuccess) return cuda_status(e, "ut_project_minmax memset");
+  const bool vector_ok = cube->row_stride == cube->cols;
+  ProjParams p{};
+  p.data = cube->data;
+  p.bs = cube->band_stride;
+  p.rs = cube->row_stride;
+  p.rows = cube->rows;
+  p.cols = cube->cols;
+  p.npix = cube->rows * cube->cols;
+  p.bands = cube->bands;
+  p.ktotal = k;
+  p.coef = coef;
+  p.ld_coef = ld_coef;
+  p.mean = mean;
+  p.std = std;
+  p.scores = scores;
+  p.minmax = minmax;
+  p.nonfinite = nonfinite;
+  char* base = static_cast<char*>(ws);
+  for (int g = 0, k0 = 0; k0 < k; ++g, k0 += kMaxGroup) {
+    const int kg = (k - k0) < kMaxGroup ? (k - k0) : kMaxGroup;
+    p.k0 = k0;
+    for (int i = 0; i < kg; ++i) p.comps[i] = components[k0 + i];
+    p.counter = reinterpret_cast<unsigned int*>(base) + g;
+    p.part = reinterpret_cast<float*>(base + 256) + (size_t)g * kMaxGrid * (2 * kMaxGroup + 1);
+    const int rc = precision ? launch_prec<true>(p, cube->dtype, kg, vector_ok, st)
+                             : launch_prec<false>(p, cube->dtype, kg, vector_ok, st);
+    if (rc != UT_OK) return rc;
+  }
+  return UT_OK;
+}
+
+int ut_stretch(const float* scores, const float* minmax, int32_t k, int32_t ld_minmax, int64_t npix,
+               int32_t depth, void* codes, void* stream) {
+  UT_REQUIRE(k >= 1 && k <= kMaxBands, "ut_stretch: k must be 1..32");
+  UT_REQUIRE(ld_minmax >= k, "ut_stretch: ld_minmax must be >= k");
+  UT_REQUIRE(depth == 8 || depth == 16, "unsupported bit depth %d; expected 8 or 16", depth);
+  if (npix <= 0) return UT_OK;
+  cudaStream_t st = as_stream(stream);
+  const bool vec16 = (npix % 16 == 0) && (reinterpret_cast<uintptr_t>(scores) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(codes) % 16 == 0);
+  const int64_t units = vec16 ? (int64_t)k * npix / 16 : (int64_t)k * npix;
+  int64_t grid = (units + kThreads - 1) / kThreads;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  if (depth == 8)
+    stretch_kernel<8><<<(int)grid, kThreads, 0, st>>>(scores, minmax, k, ld_minmax, npix, codes, vec16);
+  else
+    stretch_kernel<16><<<(int)grid, kThreads, 0, st>>>(scores, minmax, k, ld_minmax, npix, codes, vec16);
+  UT_CHECK_LAUNCH("stretch_kernel");
+  return UT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,212 @@
+"""Device-resident fused CVA / PCA pipelines (the measured hot path).
+
+One ``run()`` enqueues the whole path on the current stream with no host
+synchronization:
+
+  CVA:  K1 gather -> K1 class moments -> [all_gather] -> K3 cva_solve
+        -> K4 project+min/max -> [all_reduce MAX] -> K5 stretch
+  PCA:  K2 region moments -> [all_gather] -> K3 pca_solve
+        -> K4 project+min/max -> [all_reduce MAX] -> K5 stretch
+
+Row sharding: each rank holds rows [row0, row0+rows) of the
+cube; training points are routed to the rank owning their row; the only data
+exchanged are the per-class moment records (all_gather, then a fixed
+rank-order combine inside the K3 kernel -- deterministic for a given world
+size) and the 2K min/max record (all_reduce MAX).  Errors found on the device
+(bad point, non-PD scatter, NaN scores) are read back by ``check()``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from . import device as dev
+from .annotations import check_points, gather
+from .eigen import DEFAULT_RIDGE, raise_for_info
+from .errors import DataError
+from .projection import (CvaDevice, PcaDevice, ProjectionModel, METHOD_CVA,
+                         METHOD_PCA_UNSUPERVISED, class_index, project_device, _top_k)
+from .rendering import stretch_planes
+from .stack import DeviceStack
+
+
+def row_bounds(height: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous row block of ``rank``: [rank*H/G, (rank+1)*H/G)."""
+    return (height * rank) // world, (height * (rank + 1)) // world
+
+
+def route_points(ys, row0: int, rows: int) -> np.ndarray:
+    """Indices (in original order) of the training points owned by a shard."""
+    ys = np.asarray(ys)
+    return np.flatnonzero((ys >= row0) & (ys < row0 + rows))
+
+
+class _Sharded:
+    def __init__(self, group):
+        self.group = group
+        self.world = dist.get_world_size(group) if group is not None else 1
+
+    def gather_moments(self, fit):
+        if self.world > 1:
+            dist.all_gather_into_tensor(fit.moments, fit.local_moments(), group=self.group)
+
+    def reduce_minmax(self, minmax):
+        if self.world > 1:
+            dist.all_reduce(minmax, op=dist.ReduceOp.MAX, group=self.group)
+
+
+class CvaPipeline(_Sharded):
+    """CVA fit + projection + stretch of one (shard of a) device cube."""
+
+    def __init__(self, stack: DeviceStack, xs, ys, labels, k: int | None = None,
+                 ridge: float = DEFAULT_RIDGE, precision: str | None = None, depth: int = 8,
+                 group=None):
+        super().__init__(group)
+        if not stack.normalized:
+            raise DataError("assemble_matrix requires a normalized stack")
+        self.ds = stack
+        self.device = stack.planes.device
+        xs, ys, labels = (np.asarray(a) for a in (xs, ys, labels))
+        if len(xs) == 0:
+            raise DataError("training set has no points")
+        check_points(xs, ys, stack.width, 0, stack.full_height)
+        self.class_ids, cls = class_index(labels)
+        if len(self.class_ids) < 2:
+            raise DataError(f"scatter needs at least 2 classes with points, got {len(self.class_ids)}")
+        self.k = _top_k(k, stack.band_count)
+        self.ridge, self.precision, self.depth = float(ridge), precision, depth
+        own = route_points(ys, stack.row0, stack.height) if self.world > 1 else np.arange(len(xs))
+        self.n = len(own)
+        b = stack.band_count
+        with torch.cuda.device(self.device):
+            xy = np.stack([xs[own], ys[own]], axis=1).astype(np.int32) if self.n else \
+                np.zeros((1, 2), np.int32)
+            self.xy = dev.to_device(xy, self.device)
+            self.cls = dev.to_device(cls[own] if self.n else np.zeros(1, np.int32), self.device)
+            self.fit = CvaDevice(b, len(self.class_ids), self.device, groups=self.world)
+            self.values = torch.empty((b, max(self.n, 1)), dtype=torch.float64, device=self.device)
+            self.first_bad = torch.full((1,), -1, dtype=torch.int64, device=self.device)
+            self.scores = torch.empty((self.k, stack.height, stack.width), dtype=torch.float32,
+                                      device=self.device)
+            self.minmax = torch.empty(2 * self.k, dtype=torch.float32, device=self.device)
+            self.nonfinite = torch.zeros(1, dtype=torch.int32, device=self.device)
+            self.codes = torch.empty((self.k, stack.height, stack.width),
+                                     dtype=torch.uint8 if depth == 8 else torch.uint16,
+                                     device=self.device)
+            self.evecs = self.fit.views["evecs"].view(b, b)
+            self.mean = self.fit.views["grand_mean"]
+
+    # -- the hot path -------------------------------------------------------
+    def fit_only(self):
+        L = _lib.lib()
+        if self.n:
+            _lib.check(L.ut_gather(self.ds.cube(), self.xy.data_ptr(), self.n,
+                                   self.values.data_ptr(), self.values.shape[1],
+                                   self.first_bad.data_ptr(), dev.stream_handle()), "ut_gather")
+        self.fit.moments_from(self.values, self.values.shape[1], self.cls, self.n)
+        self.gather_moments(self.fit)
+        self.fit.solve(self.ridge)
+
+    def project_only(self):
+        project_device(self.ds, self.evecs, self.mean, None, range(self.k), self.precision,
+                       self.scores, self.minmax, self.nonfinite)
+        self.reduce_minmax(self.minmax)
+
+    def stretch_only(self):
+        stretch_planes(self.scores, self.minmax, self.depth, out=self.codes)
+
+    def run(self):
+        with torch.cuda.device(self.device):
+            self.fit_only()
+            self.project_only()
+            self.stretch_only()
+        return self.codes
+
+    # -- results ------------------------------------------------------------
+    def check(self):
+        """Synchronize and raise the reference's errors for device-side failures."""
+        if int(self.first_bad.item()) >= 0:
+            raise DataError(f"training point {int(self.first_bad.item())} outside the stack")
+        h = self.fit.host()
+        raise_for_info(h["info"], h["aux"])
+        if int(self.nonfinite.item()):
+            raise DataError("score plane contains NaN or Inf")
+        return h
+
+    def model(self) -> ProjectionModel:
+        h = self.check()
+        return ProjectionModel(method=METHOD_CVA, mean=h["grand_mean"], std=None,
+                               coefficients=np.ascontiguousarray(h["evecs"][:, :self.k]),
+                               eigenvalues=np.ascontiguousarray(h["evals"][:self.k]))
+
+    def launches(self) -> int:
+        """Our kernels per run(): gather, 2x moments, solve, K4 groups, stretch."""
+        return (1 if self.n else 0) + (2 if self.n else 0) + 1 + (self.k + 7) // 8 + 1
+
+
+class PcaPipeline(_Sharded):
+    """Unsupervised PCA fit + projection + stretch of one (shard of a) device cube."""
+
+    def __init__(self, stack: DeviceStack, k: int | None = None, precision: str | None = None,
+                 depth: int = 8, group=None):
+        super().__init__(group)
+        self.ds = stack
+        self.device = stack.planes.device
+        self.k = _top_k(k, stack.band_count)
+        if stack.full_height * stack.width < 2:
+            raise DataError("unsupervised PCA needs at least 2 pixels")
+        self.precision, self.depth = precision, depth
+        b = stack.band_count
+        with torch.cuda.device(self.device):
+            self.fit = PcaDevice(b, self.device, groups=self.world)
+            self.scores = torch.empty((self.k, stack.height, stack.width), dtype=torch.float32,
+                                      device=self.device)
+            self.minmax = torch.empty(2 * self.k, dtype=torch.float32, device=self.device)
+            self.nonfinite = torch.zeros(1, dtype=torch.int32, device=self.device)
+            self.codes = torch.empty((self.k, stack.height, stack.width),
+                                     dtype=torch.uint8 if depth == 8 else torch.uint16,
+                                     device=self.device)
+            self.evecs = self.fit.views["evecs"].view(b, b)
+
+    def fit_only(self):
+        if self.ds.height:
+            self.fit.moments_from(self.ds.cube(), 0, 0, self.ds.width, self.ds.height, self.device)
+        else:
+            self.fit.local_moments().zero_()
+        self.gather_moments(self.fit)
+        self.fit.solve()
+
+    def project_only(self):
+        project_device(self.ds, self.evecs, self.fit.views["mean"], self.fit.views["std"],
+                       range(self.k), self.precision, self.scores, self.minmax, self.nonfinite)
+        self.reduce_minmax(self.minmax)
+
+    def stretch_only(self):
+        stretch_planes(self.scores, self.minmax, self.depth, out=self.codes)
+
+    def run(self):
+        with torch.cuda.device(self.device):
+            self.fit_only()
+            self.project_only()
+            self.stretch_only()
+        return self.codes
+
+    def check(self):
+        h = self.fit.host()
+        raise_for_info(h["info"], None)
+        if int(self.nonfinite.item()):
+            raise DataError("score plane contains NaN or Inf")
+        return h
+
+    def model(self) -> ProjectionModel:
+        h = self.check()
+        return ProjectionModel(method=METHOD_PCA_UNSUPERVISED, mean=h["mean"], std=h["std"],
+                               coefficients=np.ascontiguousarray(h["evecs"][:, :self.k]),
+                               eigenvalues=np.ascontiguousarray(h["evals"][:self.k]))
+
+    def launches(self) -> int:
+        """shift + region moments, solve, K4 groups, stretch."""
+        return 2 + 1 + (self.k + 7) // 8 + 1

@@ -1,0 +1,167 @@
+"""Spectral cubes on the host and in HBM.
+
+``SpectralStack`` mirrors the reference container
+(/root/reference/pkg/src/undertext/stack.py:22-98): B co-registered planes,
+(B, H, W) band-sequential, read-only, with per-band metadata.  ``DeviceStack``
+is the same cube resident in HBM (a torch tensor), optionally a row shard
+``[row0, row0 + rows)`` of a taller image; it is what the fast path consumes.
+A host stack is staged to HBM once and the device copy is cached for the
+lifetime of its (immutable) plane array, so the reference's usual call
+sequence -- assemble_matrix, fit, project_stack on one stack -- pays one H2D.
+"""
+
+from __future__ import annotations
+
+import threading
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import device as dev
+from .errors import DataError
+
+
+@dataclass(frozen=True)
+class BandMeta:
+    """Acquisition metadata for one band (stack.py:22-36)."""
+
+    band_id: int
+    wavelength_nm: float
+    illumination: str
+    filter: str | None = None
+
+    def __post_init__(self):
+        if self.wavelength_nm <= 0:
+            raise DataError(f"band {self.band_id}: wavelength must be positive, "
+                            f"got {self.wavelength_nm}")
+
+
+def default_bands(n: int) -> tuple[BandMeta, ...]:
+    return tuple(BandMeta(i, 400.0 + i, "synthetic") for i in range(n))
+
+
+@dataclass(frozen=True)
+class SpectralStack:
+    """Host cube, validated like the reference (stack.py:53-71)."""
+
+    bands: tuple[BandMeta, ...]
+    planes: np.ndarray = field(repr=False)
+    bit_depth: int
+    normalized: bool = False
+
+    def __post_init__(self):
+        if self.bit_depth not in (8, 16):
+            raise DataError(f"bit depth must be 8 or 16, got {self.bit_depth}")
+        if self.planes.ndim != 3 or self.planes.shape[0] != len(self.bands):
+            raise DataError(f"planes shape {self.planes.shape} does not match "
+                            f"{len(self.bands)} bands")
+        if len(self.bands) < 1:
+            raise DataError("a stack needs at least one band")
+        ids = [b.band_id for b in self.bands]
+        if len(set(ids)) != len(ids):
+            raise DataError(f"duplicate band ids in stack: {ids}")
+        if self.planes.size and float(self.planes.max()) >= (1 << self.bit_depth):
+            raise DataError(f"sample value {self.planes.max()} exceeds "
+                            f"{self.bit_depth}-bit range")
+        self.planes.setflags(write=False)
+
+    @property
+    def band_count(self) -> int:
+        return len(self.bands)
+
+    @property
+    def width(self) -> int:
+        return int(self.planes.shape[2])
+
+    @property
+    def height(self) -> int:
+        return int(self.planes.shape[1])
+
+
+@dataclass(frozen=True)
+class DeviceStack:
+    """A cube (or row shard) resident in HBM.
+
+    ``planes`` is a (B, rows, W) CUDA tensor of uint8/uint16/float16/float32/
+    float64 samples; ``row0`` is the global index of local row 0 and
+    ``full_height`` the global image height (== rows when unsharded).
+    """
+
+    bands: tuple[BandMeta, ...]
+    planes: torch.Tensor = field(repr=False)
+    bit_depth: int = 8
+    normalized: bool = True
+    row0: int = 0
+    full_height: int | None = None
+
+    def __post_init__(self):
+        if not self.planes.is_cuda:
+            raise DataError("DeviceStack planes must be a CUDA tensor")
+        if self.planes.dim() != 3 or self.planes.shape[0] != len(self.bands):
+            raise DataError(f"planes shape {tuple(self.planes.shape)} does not match "
+                            f"{len(self.bands)} bands")
+        if self.planes.dtype not in dev.TORCH_TO_UT:
+            raise DataError(f"unsupported sample dtype {self.planes.dtype}")
+        if self.full_height is None:
+            object.__setattr__(self, "full_height", int(self.planes.shape[1]) + self.row0)
+
+    @property
+    def band_count(self) -> int:
+        return len(self.bands)
+
+    @property
+    def width(self) -> int:
+        return int(self.planes.shape[2])
+
+    @property
+    def height(self) -> int:
+        """Local rows (the reference's stack.height for an unsharded stack)."""
+        return int(self.planes.shape[1])
+
+    @property
+    def pixels(self) -> int:
+        return self.height * self.width
+
+    def cube(self):
+        return dev.cube_desc(self.planes, self.row0)
+
+    @classmethod
+    def from_host(cls, stack: SpectralStack, device=None) -> "DeviceStack":
+        device = device or dev.require_cuda()
+        t = torch.from_numpy(np.ascontiguousarray(stack.planes))
+        return cls(stack.bands, t.to(device), stack.bit_depth, stack.normalized)
+
+
+_cache_lock = threading.Lock()
+_device_copies: dict[int, tuple[weakref.ref, DeviceStack]] = {}
+
+
+def on_device(stack) -> DeviceStack:
+    """The HBM copy of a stack (identity for a DeviceStack; cached H2D otherwise)."""
+    if isinstance(stack, DeviceStack):
+        return stack
+    if not isinstance(stack, SpectralStack):
+        raise DataError(f"expected a SpectralStack or DeviceStack, got {type(stack).__name__}")
+    device = dev.require_cuda()
+    key = id(stack.planes)
+    with _cache_lock:
+        hit = _device_copies.get(key)
+        if hit is not None and hit[0]() is stack.planes and \
+                hit[1].planes.device == device and hit[1].normalized == stack.normalized:
+            return hit[1]
+    ds = DeviceStack.from_host(stack, device)
+    with _cache_lock:
+        ref = weakref.ref(stack.planes, lambda _r, k=key: _device_copies.pop(k, None)) \
+            if _weakrefable(stack.planes) else (lambda: None)
+        _device_copies[key] = (ref, ds)
+    return ds
+
+
+def _weakrefable(a) -> bool:
+    try:
+        weakref.ref(a)
+        return True
+    except TypeError:
+        return False

@@ -1,0 +1,51 @@
+"""CPU checks of the C-ABI library: it loads, and exports every symbol the
+header declares.  No compute calls (no GPU here)."""
+
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "undertext_b200.h"
+
+
+def declared():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|int64_t|const char\*)\s+(ut_\w+)\(", text, re.M)))
+
+
+def test_header_and_binding_agree():
+    from paper_1612_06457_b200 import _lib
+
+    assert sorted(_lib.EXPORTS) == declared()
+
+
+def test_library_exports_every_symbol():
+    from paper_1612_06457_b200 import _lib
+
+    if not _lib.LIB_PATH.exists():
+        pytest.skip("library not built (run __graft_entry__.build())")
+    handle = _lib.lib()
+    for name in declared():
+        assert hasattr(handle, name), name
+    assert handle.ut_version() == 1
+    assert handle.ut_moment_len(32) == 1 + 32 + 32 * 32
+    assert handle.ut_project_ws() > 0
+    assert handle.ut_class_moments_ws(60000, 32, 6) > 60000 // 128 * 6 * 33 * 8
+    assert handle.ut_region_moments_ws(32) > 0
+    assert handle.ut_plane_minmax_ws() > 0
+
+
+def test_library_is_sm100a():
+    """The shipped cubin targets sm_100a (cuobjdump lists the ELF arch)."""
+    import shutil
+    import subprocess
+
+    from paper_1612_06457_b200 import _lib
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not _lib.LIB_PATH.exists() or not Path(tool).exists():
+        pytest.skip("library or cuobjdump missing")
+    out = subprocess.run([tool, "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
