@@ -46,8 +46,8 @@ def to_device(arr, device, dtype=None) -> torch.Tensor:
         t = arr
     else:
         a = np.ascontiguousarray(arr)
-        if a.dtype not in NUMPY_TO_TORCH and a.dtype.kind in "iu":
-            a = a.astype(np.int64)
+        if not a.flags.writeable:
+            a = a.copy()
         t = torch.from_numpy(a)
     if dtype is not None:
         t = t.to(dtype)
