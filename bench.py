@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""Benchmark of the CVA hot path (BASELINE.json metric: CVA Mpixel/s,
+scatter + eigen + projection, at 1/2/4/8 B200, and % of HBM roofline).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+  python bench.py --impl reference ...     # the reference algorithm on host cores
+
+A step is one full pass of the hot path over the synthetic cube already in
+HBM: K1 gather + class moments -> K3 scatter/eigen -> K4 projection + min/max
+-> K5 uint8 stretch (for N > 1 plus the moment all_gather and the min/max
+all_reduce over NCCL).  Rank 0 prints one JSON line.  See DESIGN.md §7.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+
+
+def hbm_peak():
+    try:
+        doc = json.loads(PEAKS_FILE.read_text())
+        return float(doc["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--rows", type=int, default=None, help="override image height (profiling)")
+    ap.add_argument("--precision", default=None, choices=[None, "fp32", "fp64"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="target CPU work for the cpu_baseline sample")
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="seconds for the whole --impl reference run")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/ut_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), float(parts[3]), parts[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3]) if v.lower() == "active"})
+        loaded = [r for r in rows if r[2] > 250.0] or rows
+        return {"sm_mhz": float(np.median([r[0] for r in loaded])),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(r[2] for r in rows)}
+
+
+# ------------------------------------------------------------------ helpers
+
+def dist_setup(n):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def pipe_precision(args):
+    from paper_1612_06457_b200 import projection
+
+    return args.precision or projection.PRECISION
+
+
+def cfg_of(args):
+    from paper_1612_06457_b200 import synthetic
+
+    cfg = synthetic.CONFIGS[args.config]
+    if args.rows:
+        cfg = synthetic.scaled(cfg, args.rows, cfg.width)
+    return cfg
+
+
+def host_cube(stack):
+    """Pinned host copy of the device cube (setup; used by e2e and the CPU arms)."""
+    import torch
+
+    host = torch.empty(stack.planes.shape, dtype=stack.planes.dtype, pin_memory=True)
+    host.copy_(stack.planes)
+    return host
+
+
+def cpu_reference(cube_np, scene, cfg, rows, workers, threads_note):
+    """One bounded sample of the workload through the oracle port of the
+    reference: assemble + fit_cva on the full training set, then project +
+    rescale_full of `rows` image rows.  Returns (seconds, pixels)."""
+    import oracle
+
+    t0 = time.perf_counter()
+    if cfg.method == "cva":
+        values = oracle.assemble(cube_np, scene.xs, scene.ys)
+        model = oracle.fit_cva(values, scene.labels, k=cfg.k)
+    else:
+        model = oracle.fit_pca_unsupervised(cube_np, k=cfg.k)
+    sample = cube_np[:, :rows]
+    scores = oracle.project(sample, model, workers=workers)
+    _ = [oracle.rescale_full(s) for s in scores]
+    return time.perf_counter() - t0, rows * cfg.width
+
+
+def cpu_threads():
+    n = len(os.sched_getaffinity(0))
+    try:
+        from threadpoolctl import threadpool_info
+
+        blas = max((i.get("num_threads", 0) for i in threadpool_info()), default=n)
+    except Exception:
+        blas = n
+    return n, blas
+
+
+def pick_rows(cube_np, scene, cfg, workers, seconds):
+    """Rows so that one sample takes about `seconds` of CPU time."""
+    probe = max(16, min(cfg.height, 256))
+    t, px = cpu_reference(cube_np, scene, cfg, probe, workers, None)
+    t_fit, _ = cpu_reference(cube_np, scene, cfg, 1, workers, None)
+    per_row = max((t - t_fit) / probe, 1e-6)
+    rows = int(max(16, min(cfg.height, (seconds - t_fit) / per_row)))
+    return rows
+
+
+# ------------------------------------------------------------------ arms
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (numpy port in oracle/, the
+    reference itself is Python and cannot travel) on this box's host cores."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import torch
+
+    from paper_1612_06457_b200 import synthetic
+
+    cfg = cfg_of(args)
+    scene = synthetic.make_scene(cfg)
+    torch.cuda.set_device(0)
+    stack = synthetic.generate(scene)      # data generation only (setup)
+    cube_np = host_cube(stack).numpy()
+    del stack
+    torch.cuda.empty_cache()
+    cores, blas = cpu_threads()
+    steps = args.steps + args.warmup
+    rows = pick_rows(cube_np, scene, cfg, cores, args.ref_budget / max(steps, 1))
+    times = []
+    for i in range(steps):
+        t, px = cpu_reference(cube_np, scene, cfg, rows, cores, None)
+        if i >= args.warmup:
+            times.append(t)
+    sec = float(np.mean(times))
+    value = px / sec / 1e6
+    sample = (f"fit on all {len(scene.xs)} training px + project/stretch of {rows} of "
+              f"{cfg.height} rows ({px} px) per step; numpy port of the reference "
+              f"(oracle/cva_pca.py), workers={cores}, BLAS threads={blas}")
+    line = {
+        "metric": "CVA Mpixel/s (scatter+eigen+projection)" if cfg.method == "cva"
+        else "PCA Mpixel/s (covariance+eigen+projection)",
+        "value": round(value, 3), "unit": "Mpixel/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "bands": cfg.bands, "classes": cfg.classes,
+                   "components": cfg.k, "pixels": cfg.pixels},
+        "cpu_baseline": {"value": round(value, 3), "unit": "Mpixel/s", "cores": cores,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args):
+    import torch
+
+    import paper_1612_06457_b200 as ut
+    from paper_1612_06457_b200 import synthetic
+
+    world, rank, local = dist_setup(args.gpus)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+
+        group = dist.group.WORLD
+    cfg = cfg_of(args)
+    scene = synthetic.make_scene(cfg)
+    r0, r1 = ut.row_bounds(cfg.height, world, rank)
+    stack = synthetic.generate(scene, row0=r0, rows=r1 - r0)
+    if cfg.method == "cva":
+        pipe = ut.CvaPipeline(stack, scene.xs, scene.ys, scene.labels, k=cfg.k,
+                              precision=args.precision, group=group)
+    else:
+        pipe = ut.PcaPipeline(stack, k=cfg.k, precision=args.precision, group=group)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        pipe.run()
+    torch.cuda.synchronize()
+    pipe.check()
+
+    # ---- timed region: K full steps, events on the launching stream
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier(world)
+        torch.cuda.synchronize()
+        start.record(stream)
+        for i in range(args.steps):
+            e = ev[i]
+            e[0].record(stream)
+            pipe.fit_only()
+            e[1].record(stream)
+            pipe.project_kernel()
+            e[2].record(stream)
+            pipe.reduce_minmax(pipe.minmax)
+            pipe.stretch_only()
+            e[3].record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    pipe.check()
+    total_ms = start.elapsed_time(stop)
+    ms_step = max_over_ranks(total_ms / args.steps, world)
+    k4_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    fit_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+    tail_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
+    k4_ms = max_over_ranks(k4_ms, world)
+
+    pixels = cfg.pixels
+    value = pixels / (ms_step * 1e-3) / 1e6
+    peak, peak_src = hbm_peak()
+    local_px = stack.pixels
+    per_px = cfg.bytes_per_pixel()
+    achieved = per_px * local_px / (k4_ms * 1e-3) / 1e9
+    step_achieved = per_px * local_px / (ms_step * 1e-3) / 1e9
+
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    if prof.exists():
+        try:
+            doc = json.loads(prof.read_text())
+            ent = doc.get(cfg.name.split("@")[0]) or {}
+            if "bytes_per_pixel" in ent:
+                traffic = round(ent["bytes_per_pixel"] * local_px / 1e9, 3)
+        except Exception:
+            traffic = None
+
+    # ---- e2e: host (pinned) cube in, uint8 planes out, through the same API
+    e2e = None
+    if not args.no_e2e:
+        host = host_cube(stack)
+        codes_host = torch.empty(pipe.codes.shape, dtype=pipe.codes.dtype, pin_memory=True)
+        h2d = host.numel() * host.element_size() + pipe.xy.numel() * 4 + pipe.cls.numel() * 4 \
+            if cfg.method == "cva" else host.numel() * host.element_size()
+        d2h = codes_host.numel() * codes_host.element_size()
+        times = []
+        for i in range(args.e2e_steps + 1):
+            barrier(world)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            stack.planes.copy_(host, non_blocking=True)
+            pipe.run()
+            codes_host.copy_(pipe.codes, non_blocking=True)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i:
+                times.append(a.elapsed_time(b))
+        e2e_ms = max_over_ranks(float(np.mean(times)), world)
+        e2e = {"value": round(pixels / (e2e_ms * 1e-3) / 1e6, 3), "unit": "Mpixel/s",
+               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+               "ms_per_step": round(e2e_ms, 3)}
+        pipe.check()
+    else:
+        host = None
+
+    # ---- CPU baseline (rank 0, N = 1): oracle port on a bounded sample
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        if host is None:
+            host = host_cube(stack)
+        cube_np = host.numpy()
+        cores, blas = cpu_threads()
+        rows = pick_rows(cube_np, scene, cfg, cores, args.cpu_seconds)
+        t, px = cpu_reference(cube_np, scene, cfg, rows, cores, None)
+        cpu = {"value": round(px / t / 1e6, 3), "unit": "Mpixel/s", "cores": cores,
+               "kind": "port",
+               "sample": (f"fit on all {len(scene.xs)} training px + project/stretch of "
+                          f"{rows}/{cfg.height} rows ({px} px), numpy port of the reference "
+                          f"(oracle/), workers={cores}, BLAS threads={blas}, {t:.1f} s")}
+
+    if rank == 0:
+        launches = pipe.launches() * args.steps
+        line = {
+            "metric": "CVA Mpixel/s (scatter+eigen+projection)" if cfg.method == "cva"
+            else "PCA Mpixel/s (covariance+eigen+projection)",
+            "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak" if world > 1 else "weak",
+            "vs_baseline": None,
+            "dtype": "f64" if pipe_precision(args) == "fp64" else "f32 (fit f64)",
+            "data": "synthetic (BASELINE.json generator, generated in HBM; seed %d)" % cfg.seed,
+            "config": {"workload": cfg.name, "height": cfg.height, "width": cfg.width,
+                       "bands": cfg.bands, "sample": str(cfg.dtype).replace("torch.", ""),
+                       "classes": cfg.classes, "training_px": int(len(scene.xs)),
+                       "components": cfg.k, "parallelism": f"rows{world}",
+                       "l2": "inputs > L2 (cube %.1f GB per GPU)" %
+                             (stack.planes.numel() * stack.planes.element_size() / 1e9)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic, "kernel": "project_kernel (K4)",
+                         "kernel_ms": round(k4_ms, 4), "bytes_per_px": per_px,
+                         "peak_source": peak_src},
+            "roofline_step": {"achieved": round(step_achieved, 1), "frac":
+                              round(step_achieved / peak, 4),
+                              "split_ms": {"fit": round(fit_ms, 4), "project": round(k4_ms, 4),
+                                           "minmax+stretch": round(tail_ms, 4)}},
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -110,9 +110,12 @@ class CvaPipeline(_Sharded):
         self.gather_moments(self.fit)
         self.fit.solve(self.ridge)
 
-    def project_only(self):
+    def project_kernel(self):
         project_device(self.ds, self.evecs, self.mean, None, range(self.k), self.precision,
                        self.scores, self.minmax, self.nonfinite)
+
+    def project_only(self):
+        self.project_kernel()
         self.reduce_minmax(self.minmax)
 
     def stretch_only(self):
@@ -179,9 +182,12 @@ class PcaPipeline(_Sharded):
         self.gather_moments(self.fit)
         self.fit.solve()
 
-    def project_only(self):
+    def project_kernel(self):
         project_device(self.ds, self.evecs, self.fit.views["mean"], self.fit.views["std"],
                        range(self.k), self.precision, self.scores, self.minmax, self.nonfinite)
+
+    def project_only(self):
+        self.project_kernel()
         self.reduce_minmax(self.minmax)
 
     def stretch_only(self):
