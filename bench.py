@@ -185,8 +185,8 @@ def cpu_reference(cube_np, scene, cfg, rows, workers, threads_note):
     if cfg.method == "cva":
         values = oracle.assemble(cube_np, scene.xs, scene.ys)
         model = oracle.fit_cva(values, scene.labels, k=cfg.k)
-    else:
-        model = oracle.fit_pca_unsupervised(cube_np, k=cfg.k)
+    else:  # PCA: the covariance pass is per pixel too -> fit on the sampled rows
+        model = oracle.fit_pca_unsupervised(cube_np[:, :max(rows, 2)], k=cfg.k)
     sample = cube_np[:, :rows]
     scores = oracle.project(sample, model, workers=workers)
     _ = [oracle.rescale_full(s) for s in scores]

@@ -109,13 +109,25 @@ int ut_class_moments(const double* values, int64_t ld, const int32_t* cls,
                      int64_t n, int32_t bands, int32_t classes, double* moments,
                      void* ws, size_t ws_bytes, void* stream);
 
+/* Fused gather + class moments straight from the cube (the pipeline form of
+ * assemble_matrix + compute_scatter): xy as for ut_gather; points outside the
+ * (shard of the) cube are skipped and reported in first_bad (-1 if none). */
+int ut_cube_class_moments(const ut_cube* cube, const int32_t* xy, const int32_t* cls,
+                          int64_t n, int32_t classes, double* moments,
+                          int64_t* first_bad, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------- K3: CVA solve
  * Combines `groups` partial moment sets (rank-major [groups][classes][len],
  * e.g. all-gathered from row shards) with the parallel-axis rule, builds the
  * symmetrized within / between scatter (projection.py:190-200), then solves
- * between v = lambda (within + ridge*tr/B*I) v in one CTA (eigen.py:63-113). */
+ * between v = lambda (within + ridge*tr/B*I) v in one CTA (eigen.py:63-113).
+ * want = number of leading eigenvectors the caller needs (<= 0: all).  When
+ * want <= (classes with points) - 1 the rank of S_b is exploited: only a C x C
+ * eigenproblem is solved, evals beyond C are exact zeros and evecs columns
+ * >= want are zero; otherwise all B pairs are computed. */
 int ut_cva_solve(const double* moments, int32_t groups, int32_t bands,
-                 int32_t classes, double ridge, const ut_cva_out* out, void* stream);
+                 int32_t classes, double ridge, int32_t want, const ut_cva_out* out,
+                 void* stream);
 
 /* ------------------------------------------------- K3: eigensolver
  * solve_gen_eig_sym(A, M, ridge) (eigen.py:75-113).  M == NULL selects the

@@ -23,7 +23,7 @@ INFO_OK, INFO_ASYM_A, INFO_ASYM_M, INFO_NOT_PD, INFO_NO_CONVERGE = 0, 1, 2, 3, 4
 # every symbol include/undertext_b200.h declares (checked by the CPU tests)
 EXPORTS = (
     "ut_version", "ut_last_error", "ut_moment_len", "ut_gather", "ut_class_moments_ws",
-    "ut_class_moments", "ut_cva_solve", "ut_gen_eig_sym", "ut_region_moments_ws",
+    "ut_class_moments", "ut_cube_class_moments", "ut_cva_solve", "ut_gen_eig_sym", "ut_region_moments_ws",
     "ut_region_moments", "ut_pca_solve", "ut_project_ws", "ut_project_minmax",
     "ut_stretch", "ut_plane_minmax_ws", "ut_plane_minmax", "ut_linear_to_codes",
     "ut_synth_cube", "ut_class_of",
@@ -58,7 +58,8 @@ _SIGS = {
     "ut_gather": (I32, [C.POINTER(Cube), P, I64, P, I64, P, P]),
     "ut_class_moments_ws": (SZ, [I64, I32, I32]),
     "ut_class_moments": (I32, [P, I64, P, I64, I32, I32, P, P, SZ, P]),
-    "ut_cva_solve": (I32, [P, I32, I32, I32, F64, C.POINTER(CvaOut), P]),
+    "ut_cube_class_moments": (I32, [C.POINTER(Cube), P, P, I64, I32, P, P, P, SZ, P]),
+    "ut_cva_solve": (I32, [P, I32, I32, I32, F64, I32, C.POINTER(CvaOut), P]),
     "ut_gen_eig_sym": (I32, [P, P, I32, F64, P, P, P, P, P]),
     "ut_region_moments_ws": (SZ, [I32]),
     "ut_region_moments": (I32, [C.POINTER(Cube), I64, I64, I64, I64, P, P, SZ, P]),

@@ -8,31 +8,51 @@
 //  * ut_pca_solve    -- combine region moments, std / correlation
 //    (projection.py:335-337), eigh + sort + sign (projection.py:263-270).
 //
-// The reference diagonalizes with LAPACK syevd (tridiagonal QR); here a cyclic
-// parallel-order Jacobi runs in shared memory on 1024 threads (one per matrix
-// element).  Jacobi is at least as accurate (it has high relative accuracy),
-// and every step is in a fixed order, so the result is deterministic.
+// The reference diagonalizes with LAPACK syevd; here a cyclic Jacobi with
+// parallel (round-robin) ordering runs in shared memory on a team of 128
+// threads (3 named-barrier phases per round).  Cholesky and the triangular
+// solves run on one warp (lane = row or column).  Everything is fixed-order,
+// so results are deterministic.
+//
+// CVA low-rank path: S_b = H H^T with H = [sqrt(n_c) (m_c - m)] (B x C), rank
+// <= C-1.  With W' = L L^T and G = L^-1 H, the nonzero eigenpairs of
+// L^-1 S_b L^-T = G G^T are those of the C x C matrix G^T G (u = G w /
+// sqrt(lambda)), so only a C x C Jacobi is needed and the B x B one is skipped.
+// Used when the caller wants at most C-1 leading pairs and they are clearly
+// non-zero; otherwise the full path runs.
 #include "common.cuh"
 
 namespace ut {
 namespace {
 
-constexpr int N = kMaxBands;    // 32
-constexpr int LD = N + 1;       // padded row stride in shared memory
-constexpr int kThreads = N * N; // 1024
+constexpr int N = kMaxBands;     // 32
+constexpr int LD = N + 1;        // padded row stride in shared memory
+constexpr int kThreads = N * N;  // 1024 (combine steps use all of them)
+constexpr int kTeam = 128;       // Jacobi team
+constexpr int kMaxC = 32;        // classes handled by the low-rank path
 
 struct Smem {
   double a[N * LD];   // working matrix (A, then C, then Jacobi iterate)
-  double m[N * LD];   // M (then L, the Cholesky factor)
-  double x[N * LD];   // scratch for the triangular solves
+  double m[N * LD];   // M (then L)
+  double x[N * LD];   // scratch
   double v[N * LD];   // eigenvectors
+  double h[N * LD];   // H, then G = L^-1 H (B x C)
   double cs[N / 2], sn[N / 2], npp[N / 2], nqq[N / 2];
   int pp[N / 2], qq[N / 2];
   double red[kThreads / 32];
   double scal[4];
   int flag;
   int order[N];
+  int code[N];
 };
+
+template <int NT> __device__ __forceinline__ void team_sync() {
+  if constexpr (NT == 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  }
+}
 
 __device__ __forceinline__ double block_max(Smem& s, double v) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -58,35 +78,37 @@ __device__ bool is_asym(Smem& s, const double* x, int n) {
   return top != 0.0 && gap > 1e-10 * top;
 }
 
-// In-place cyclic Jacobi on s.a (n x n) with eigenvectors accumulated in s.v.
-// Parallel (round-robin) ordering: n/2 disjoint rotations per round.
-__device__ int jacobi(Smem& s, int n) {
-  const int tid = threadIdx.x;
-  const int i = tid / N, j = tid % N;
-  if (i < n && j < n) s.v[i * LD + j] = (i == j) ? 1.0 : 0.0;
+// Cyclic Jacobi on a (n x n, stride LD) with eigenvectors in v, run by threads
+// [0, NT) of the CTA (the caller parks the others at a __syncthreads).
+template <int NT>
+__device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
+  const int t = threadIdx.x;
+  for (int e = t; e < n * n; e += NT) {
+    const int i = e / n, j = e - i * n;
+    v[i * LD + j] = (i == j) ? 1.0 : 0.0;
+  }
+  // absolute floor: off-diagonals below 1e-22 * ||A||_F count as zero
+  double fro = 0.0;
+  for (int e = t; e < n * n; e += NT) {
+    const int i = e / n, j = e - i * n;
+    fro += a[i * LD + j] * a[i * LD + j];
+  }
+  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+  if ((t & 31) == 0) s.red[t >> 5] = fro;
+  team_sync<NT>();
+  double f = 0.0;
+  for (int w = 0; w < NT / 32; ++w) f += s.red[w];
+  team_sync<NT>();
+  const double floor_abs = 1e-22 * sqrt(f);
+  if (n < 2) return 0;
   const int m = n + (n & 1);
   const int half = m / 2;
-  // absolute floor: off-diagonals below 1e-22 * ||A||_F are treated as zero
-  double fro = 0.0;
-  if (i < n && j < n) fro = s.a[i * LD + j] * s.a[i * LD + j];
-  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
-  __syncthreads();
-  if ((tid & 31) == 0) s.red[tid >> 5] = fro;
-  __syncthreads();
-  if (tid == 0) {
-    double f = 0.0;
-    for (int w = 0; w < kThreads / 32; ++w) f += s.red[w];
-    s.scal[0] = 1e-22 * sqrt(f);
-  }
-  __syncthreads();
-  const double floor_abs = s.scal[0];
-  if (n < 2) return 0;
   for (int sweep = 0; sweep < 60; ++sweep) {
-    if (tid == 0) s.flag = 0;
-    __syncthreads();
+    int rotated = 0;
     for (int r = 0; r < m - 1; ++r) {
-      if (tid < half) {
-        const int k = tid;
+      // phase A: rotation of pair k (Rutishauser's stable formulas)
+      if (t < half) {
+        const int k = t;
         int p, q;
         if (k == 0) {
           p = m - 1;
@@ -95,26 +117,26 @@ __device__ int jacobi(Smem& s, int n) {
           p = (r + k) % (m - 1);
           q = (r - k + (m - 1)) % (m - 1);
         }
-        if (p > q) { const int t = p; p = q; q = t; }
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
         double c = 1.0, sn = 0.0, npp = 0.0, nqq = 0.0;
         int act = 0;
         if (q < n) {
-          const double apq = s.a[p * LD + q];
-          const double app = s.a[p * LD + p], aqq = s.a[q * LD + q];
+          const double apq = a[p * LD + q];
+          const double app = a[p * LD + p], aqq = a[q * LD + q];
           const double thr = fmax(0.5 * DBL_EPSILON * sqrt(fabs(app) * fabs(aqq)), floor_abs);
           if (fabs(apq) > thr) {
             const double theta = (aqq - app) / (2.0 * apq);
-            double t;
+            double tt;
             if (fabs(theta) > 1e150) {
-              t = 0.5 / theta;
+              tt = 0.5 / theta;
             } else {
-              t = 1.0 / (fabs(theta) + sqrt(1.0 + theta * theta));
-              if (theta < 0.0) t = -t;
+              tt = 1.0 / (fabs(theta) + sqrt(1.0 + theta * theta));
+              if (theta < 0.0) tt = -tt;
             }
-            c = 1.0 / sqrt(1.0 + t * t);
-            sn = t * c;
-            npp = app - t * apq;
-            nqq = aqq + t * apq;
+            c = 1.0 / sqrt(1.0 + tt * tt);
+            sn = tt * c;
+            npp = app - tt * apq;
+            nqq = aqq + tt * apq;
             act = 1;
           }
         }
@@ -124,111 +146,118 @@ __device__ int jacobi(Smem& s, int n) {
         s.sn[k] = sn;
         s.npp[k] = npp;
         s.nqq[k] = nqq;
-        if (act) s.flag = 1;
+        rotated |= act;
       }
-      __syncthreads();
-      // rows p, q  <- J^T A
-      if (tid < half * N) {
-        const int k = tid / N, col = tid % N;
+      team_sync<NT>();
+      // phase B: rows p, q <- J^T A
+      for (int e = t; e < half * n; e += NT) {
+        const int k = e / n, col = e - k * n;
         const int p = s.pp[k];
-        if (p >= 0 && col < n) {
-          const int q = s.qq[k];
-          const double c = s.cs[k], sn = s.sn[k];
-          const double ap = s.a[p * LD + col], aq = s.a[q * LD + col];
-          s.a[p * LD + col] = c * ap - sn * aq;
-          s.a[q * LD + col] = sn * ap + c * aq;
-        }
-      }
-      __syncthreads();
-      // columns p, q <- A J ; V <- V J
-      if (tid < half * N) {
-        const int k = tid / N, row = tid % N;
-        const int p = s.pp[k];
-        if (p >= 0 && row < n) {
-          const int q = s.qq[k];
-          const double c = s.cs[k], sn = s.sn[k];
-          const double ap = s.a[row * LD + p], aq = s.a[row * LD + q];
-          s.a[row * LD + p] = c * ap - sn * aq;
-          s.a[row * LD + q] = sn * ap + c * aq;
-          const double vp = s.v[row * LD + p], vq = s.v[row * LD + q];
-          s.v[row * LD + p] = c * vp - sn * vq;
-          s.v[row * LD + q] = sn * vp + c * vq;
-        }
-      }
-      __syncthreads();
-      if (tid < half) {
-        const int p = s.pp[tid];
         if (p >= 0) {
-          const int q = s.qq[tid];
-          s.a[p * LD + p] = s.npp[tid];
-          s.a[q * LD + q] = s.nqq[tid];
-          s.a[p * LD + q] = 0.0;
-          s.a[q * LD + p] = 0.0;
+          const int q = s.qq[k];
+          const double c = s.cs[k], sn = s.sn[k];
+          const double ap = a[p * LD + col], aq = a[q * LD + col];
+          a[p * LD + col] = c * ap - sn * aq;
+          a[q * LD + col] = sn * ap + c * aq;
         }
       }
-      __syncthreads();
+      team_sync<NT>();
+      // phase C: columns p, q <- A J (exact 2x2 block written), V <- V J
+      for (int e = t; e < half * n; e += NT) {
+        const int k = e / n, row = e - k * n;
+        const int p = s.pp[k];
+        if (p >= 0) {
+          const int q = s.qq[k];
+          const double c = s.cs[k], sn = s.sn[k];
+          if (row == p) {
+            a[p * LD + p] = s.npp[k];
+            a[p * LD + q] = 0.0;
+          } else if (row == q) {
+            a[q * LD + p] = 0.0;
+            a[q * LD + q] = s.nqq[k];
+          } else {
+            const double ap = a[row * LD + p], aq = a[row * LD + q];
+            a[row * LD + p] = c * ap - sn * aq;
+            a[row * LD + q] = sn * ap + c * aq;
+          }
+          const double vp = v[row * LD + p], vq = v[row * LD + q];
+          v[row * LD + p] = c * vp - sn * vq;
+          v[row * LD + q] = sn * vp + c * vq;
+        }
+      }
+      team_sync<NT>();
     }
-    const int rotated = s.flag;
-    __syncthreads();
-    if (!rotated) return 0;
+    // any rotation this sweep?  (team-wide OR through shared memory)
+    const int warp_any = __any_sync(0xffffffffu, rotated);
+    if ((t & 31) == 0) s.red[t >> 5] = warp_any ? 1.0 : 0.0;
+    team_sync<NT>();
+    double any = 0.0;
+    for (int w = 0; w < NT / 32; ++w) any += s.red[w];
+    team_sync<NT>();
+    if (any == 0.0) return 0;
   }
   return UT_INFO_NO_CONVERGE;
 }
 
-// Cholesky of s.m in place (lower).  Returns false if a pivot is not > 0.
-__device__ bool cholesky(Smem& s, int n) {
-  const int tid = threadIdx.x;
-  const int i = tid / N, j = tid % N;
+// Cholesky of m (lower, in place) by warp 0; false if a pivot is not > 0.
+__device__ bool chol_warp(double* m, int n) {
+  const int lane = threadIdx.x & 31;
   for (int k = 0; k < n; ++k) {
-    if (tid == 0) {
-      const double d = s.m[k * LD + k];
-      s.flag = (d > 0.0) ? 1 : 0;  // also rejects NaN
-      if (d > 0.0) s.m[k * LD + k] = sqrt(d);
+    __syncwarp();
+    const double d = m[k * LD + k];
+    if (!(d > 0.0)) return false;  // also rejects NaN (uniform across lanes)
+    const double lkk = sqrt(d);
+    __syncwarp();
+    if (lane == k) m[k * LD + k] = lkk;
+    if (lane > k && lane < n) m[lane * LD + k] /= lkk;
+    __syncwarp();
+    if (lane > k && lane < n) {
+      const double lik = m[lane * LD + k];
+      for (int j = k + 1; j <= lane; ++j) m[lane * LD + j] -= lik * m[j * LD + k];
     }
-    __syncthreads();
-    if (!s.flag) return false;
-    if (tid > k && tid < n) s.m[tid * LD + k] /= s.m[k * LD + k];
-    __syncthreads();
-    if (i > k && i < n && j > k && j <= i) s.m[i * LD + j] -= s.m[i * LD + k] * s.m[j * LD + k];
-    __syncthreads();
   }
-  if (i < n && j < n && j > i) s.m[i * LD + j] = 0.0;
-  __syncthreads();
+  __syncwarp();
+  if (lane < n)
+    for (int j = lane + 1; j < n; ++j) m[lane * LD + j] = 0.0;
+  __syncwarp();
   return true;
 }
 
-// x <- L^-1 x (forward substitution, all columns in parallel)
-__device__ void solve_lower(Smem& s, double* x, int n) {
-  const int tid = threadIdx.x;
-  const int i = tid / N, j = tid % N;
-  for (int p = 0; p < n; ++p) {
-    if (tid < n) x[p * LD + tid] /= s.m[p * LD + p];
-    __syncthreads();
-    if (i > p && i < n && j < n) x[i * LD + j] -= s.m[i * LD + p] * x[p * LD + j];
-    __syncthreads();
+// X <- L^-1 X for columns [0, cols) (lane = column), warp 0
+__device__ void fsolve_warp(const double* L, double* X, int n, int cols) {
+  const int lane = threadIdx.x & 31;
+  if (lane < cols) {
+    for (int p = 0; p < n; ++p) {
+      double acc = X[p * LD + lane];
+      for (int q = 0; q < p; ++q) acc -= L[p * LD + q] * X[q * LD + lane];
+      X[p * LD + lane] = acc / L[p * LD + p];
+    }
   }
+  __syncwarp();
 }
 
-// x <- L^-T x (backward substitution)
-__device__ void solve_upper_t(Smem& s, double* x, int n) {
-  const int tid = threadIdx.x;
-  const int i = tid / N, j = tid % N;
-  for (int p = n - 1; p >= 0; --p) {
-    if (tid < n) x[p * LD + tid] /= s.m[p * LD + p];
-    __syncthreads();
-    if (i < p && j < n) x[i * LD + j] -= s.m[p * LD + i] * x[p * LD + j];
-    __syncthreads();
+// X[:, col] <- L^-T X[:, col] (lane -> column cols_of[lane]), warp 0
+__device__ void bsolve_warp(const double* L, double* X, int n, int cols, const int* cols_of) {
+  const int lane = threadIdx.x & 31;
+  if (lane < cols) {
+    const int c = cols_of ? cols_of[lane] : lane;
+    for (int p = n - 1; p >= 0; --p) {
+      double acc = X[p * LD + c];
+      for (int q = p + 1; q < n; ++q) acc -= L[q * LD + p] * X[q * LD + c];
+      X[p * LD + c] = acc / L[p * LD + p];
+    }
   }
+  __syncwarp();
 }
 
-// Descending order of the diagonal of s.a (stable on ties by index).
-__device__ void sort_desc(Smem& s, int n) {
+// order[r] = index of the r-th largest diagonal entry of a (stable on ties)
+__device__ void sort_desc(Smem& s, const double* a, int n) {
   const int tid = threadIdx.x;
   if (tid < n) {
-    const double me = s.a[tid * LD + tid];
+    const double me = a[tid * LD + tid];
     int rank = 0;
     for (int o = 0; o < n; ++o) {
-      const double other = s.a[o * LD + o];
+      const double other = a[o * LD + o];
       rank += (other > me) || (other == me && o < tid);
     }
     s.order[rank] = tid;
@@ -236,65 +265,89 @@ __device__ void sort_desc(Smem& s, int n) {
   __syncthreads();
 }
 
-// Write eigenvalues/vectors in sorted order, sign-normalized (eigen.py:40-52:
-// the first entry of largest magnitude is made positive).
-__device__ void emit(Smem& s, const double* vec, int n, double* evals, double* evecs) {
+// Write nval sorted eigenvalues and `cols` sign-normalized vectors of length b
+// (first largest-|entry| made positive, eigen.py:40-52); vector r is column
+// s.order[r] of vec.  evecs columns >= cols are written as zeros.
+__device__ void emit(Smem& s, const double* a, const double* vec, int b, int nval, int cols,
+                     double* evals, double* evecs) {
   const int tid = threadIdx.x;
   const int i = tid / N, j = tid % N;
-  if (tid < n) {
+  if (tid < nval) {
     const int src = s.order[tid];
-    evals[tid] = s.a[src * LD + src];
-    int lead = 0;
-    double best = -1.0;
-    for (int r = 0; r < n; ++r) {
-      const double mag = fabs(vec[r * LD + src]);
-      if (mag > best) { best = mag; lead = r; }
+    evals[tid] = a[src * LD + src];
+    int c = src + 1;
+    if (tid < cols) {
+      int lead = 0;
+      double best = -1.0;
+      for (int r = 0; r < b; ++r) {
+        const double mag = fabs(vec[r * LD + src]);
+        if (mag > best) { best = mag; lead = r; }
+      }
+      if (vec[lead * LD + src] < 0.0) c = -c;
     }
-    s.order[tid] = (vec[lead * LD + src] < 0.0) ? -(src + 1) : (src + 1);
+    s.code[tid] = c;
   }
   __syncthreads();
-  if (i < n && j < n) {
-    const int code = s.order[j];
-    const int src = (code < 0 ? -code : code) - 1;
-    const double val = vec[i * LD + src];
-    evecs[i * n + j] = code < 0 ? -val : val;
+  if (i < b && j < b) {
+    double val = 0.0;
+    if (j < cols) {
+      const int cj = s.code[j];
+      const int src = (cj < 0 ? -cj : cj) - 1;
+      val = vec[i * LD + src];
+      if (cj < 0) val = -val;
+    }
+    evecs[i * b + j] = val;
   }
+  __syncthreads();
 }
 
-// Generalized (M != null) or standard symmetric eigenproblem on s.a / s.m.
+__device__ void ridge_into_m(Smem& s, int n, double ridge) {
+  // M' = M + ridge * (tr M / B) I, or ridge * I if tr M <= 0 (eigen.py:63-72)
+  if (threadIdx.x == 0) {
+    double tr = 0.0;
+    for (int k = 0; k < n; ++k) tr += s.m[k * LD + k];
+    s.scal[1] = ridge * (tr > 0.0 ? tr / n : 1.0);
+  }
+  __syncthreads();
+  if (threadIdx.x < n) s.m[threadIdx.x * LD + threadIdx.x] += s.scal[1];
+  __syncthreads();
+}
+
+// Full path.  Generalized (M in s.m) or standard symmetric problem on s.a.
 // Returns an info code; on NOT_PD, aux gets the eigenvalues of M'.
-__device__ int solve_pair(Smem& s, int n, bool generalized, double ridge, double* evals,
-                          double* evecs, double* aux) {
+__device__ int solve_full(Smem& s, int n, bool generalized, double ridge, bool checks,
+                          double* evals, double* evecs, double* aux) {
   const int tid = threadIdx.x;
   const int i = tid / N, j = tid % N;
   if (generalized) {
-    if (is_asym(s, s.a, n)) return UT_INFO_ASYM_A;
-    if (is_asym(s, s.m, n)) return UT_INFO_ASYM_M;
-    // ridge: M' = M + ridge * (tr M / B) I, or ridge * I if tr M <= 0
-    if (tid == 0) {
-      double tr = 0.0;
-      for (int k = 0; k < n; ++k) tr += s.m[k * LD + k];
-      s.scal[1] = ridge * (tr > 0.0 ? tr / n : 1.0);
+    if (checks) {
+      if (is_asym(s, s.a, n)) return UT_INFO_ASYM_A;
+      if (is_asym(s, s.m, n)) return UT_INFO_ASYM_M;
+    }
+    ridge_into_m(s, n, ridge);
+    if (i < n && j < n) s.x[i * LD + j] = s.m[i * LD + j];  // keep M' for the report
+    __syncthreads();
+    if (tid < 32) {
+      const bool ok = chol_warp(s.m, n);
+      if (tid == 0) s.flag = ok ? 1 : 0;
     }
     __syncthreads();
-    if (tid < n) s.m[tid * LD + tid] += s.scal[1];
-    __syncthreads();
-    // keep M' for the failure report
-    if (i < n && j < n) s.x[i * LD + j] = s.m[i * LD + j];
-    __syncthreads();
-    if (!cholesky(s, n)) {
+    if (!s.flag) {
       if (i < n && j < n) s.a[i * LD + j] = 0.5 * (s.x[i * LD + j] + s.x[j * LD + i]);
       __syncthreads();
-      jacobi(s, n);
-      sort_desc(s, n);
+      if (tid < kTeam) jacobi_team<kTeam>(s, s.a, s.v, n);
+      __syncthreads();
+      sort_desc(s, s.a, n);
       if (tid < n) aux[tid] = s.a[s.order[tid] * LD + s.order[tid]];
       return UT_INFO_NOT_PD;
     }
     // C = L^-1 A L^-T: X = L^-1 A; C = L^-1 X^T; symmetrize (eigen.py:107-109)
-    solve_lower(s, s.a, n);
+    if (tid < 32) fsolve_warp(s.m, s.a, n, n);
+    __syncthreads();
     if (i < n && j < n) s.x[i * LD + j] = s.a[j * LD + i];
     __syncthreads();
-    solve_lower(s, s.x, n);
+    if (tid < 32) fsolve_warp(s.m, s.x, n, n);
+    __syncthreads();
     if (i < n && j < n) s.a[i * LD + j] = 0.5 * (s.x[i * LD + j] + s.x[j * LD + i]);
     __syncthreads();
   } else {
@@ -303,16 +356,22 @@ __device__ int solve_pair(Smem& s, int n, bool generalized, double ridge, double
     if (i < n && j < n) s.a[i * LD + j] = s.x[i * LD + j];
     __syncthreads();
   }
-  const int info = jacobi(s, n);
-  sort_desc(s, n);
+  if (tid < kTeam) {
+    const int code = jacobi_team<kTeam>(s, s.a, s.v, n);
+    if (tid == 0) s.flag = code;
+  }
+  __syncthreads();
+  const int info = s.flag;
+  sort_desc(s, s.a, n);
   if (generalized) {
     // V = L^-T U (eigen.py:112)
     if (i < n && j < n) s.x[i * LD + j] = s.v[i * LD + j];
     __syncthreads();
-    solve_upper_t(s, s.x, n);
-    emit(s, s.x, n, evals, evecs);
+    if (tid < 32) bsolve_warp(s.m, s.x, n, n, nullptr);
+    __syncthreads();
+    emit(s, s.a, s.x, n, n, n, evals, evecs);
   } else {
-    emit(s, s.v, n, evals, evecs);
+    emit(s, s.a, s.v, n, n, n, evals, evecs);
   }
   return info;
 }
@@ -327,14 +386,64 @@ gen_eig_kernel(const double* __restrict__ A, const double* __restrict__ M, int n
     if (M) s.m[i * LD + j] = M[i * n + j];
   }
   __syncthreads();
-  const int code = solve_pair(s, n, M != nullptr, ridge, evals, evecs, aux);
+  const int code = solve_full(s, n, M != nullptr, ridge, true, evals, evecs, aux);
   if (threadIdx.x == 0) *info = code;
+}
+
+// Low-rank CVA solve (see the header comment).  Returns false (state of s.a /
+// s.m undefined) if it cannot be used; the caller then runs the full path.
+__device__ bool cva_low_rank(Smem& s, int n, int C, double ridge, int want, ut_cva_out& out) {
+  const int tid = threadIdx.x;
+  const int i = tid / N, j = tid % N;
+  ridge_into_m(s, n, ridge);
+  if (tid < 32) {
+    const bool ok = chol_warp(s.m, n);
+    if (tid == 0) s.flag = ok ? 1 : 0;
+  }
+  __syncthreads();
+  if (!s.flag) return false;
+  if (tid < 32) fsolve_warp(s.m, s.h, n, C);  // G = L^-1 H
+  __syncthreads();
+  // T = G^T G (C x C), symmetrized, in s.a
+  if (i < C && j < C) {
+    double acc = 0.0;
+    for (int p = 0; p < n; ++p) acc += s.h[p * LD + i] * s.h[p * LD + j];
+    s.x[i * LD + j] = acc;
+  }
+  __syncthreads();
+  if (i < C && j < C) s.a[i * LD + j] = 0.5 * (s.x[i * LD + j] + s.x[j * LD + i]);
+  __syncthreads();
+  if (tid < 32) {
+    const int code = jacobi_team<32>(s, s.a, s.v, C);
+    if (tid == 0) s.flag = code;
+  }
+  __syncthreads();
+  const int jinfo = s.flag;
+  sort_desc(s, s.a, C);
+  const double lmax = s.a[s.order[0] * LD + s.order[0]];
+  const double lw = s.a[s.order[want - 1] * LD + s.order[want - 1]];
+  if (jinfo != 0 || !(lmax > 0.0) || !(lw > 1e-12 * lmax)) return false;
+  // u_r = G w_r / sqrt(lambda_r), stored in column order[r] of s.x
+  if (i < n && j < want) {
+    const int src = s.order[j];
+    const double lam = s.a[src * LD + src];
+    double acc = 0.0;
+    for (int c = 0; c < C; ++c) acc += s.h[i * LD + c] * s.v[c * LD + src];
+    s.x[i * LD + src] = acc / sqrt(lam);
+  }
+  __syncthreads();
+  if (tid < 32) bsolve_warp(s.m, s.x, n, want, s.order);  // V = L^-T U
+  __syncthreads();
+  if (tid < n) out.evals[tid] = 0.0;  // the null space: exact zeros
+  __syncthreads();
+  emit(s, s.a, s.x, n, C, want, out.evals, out.evecs);
+  return true;
 }
 
 // moments: [groups][classes][1 + B + B*B] = count, mean, M2 (centred)
 __global__ void __launch_bounds__(kThreads, 1)
 cva_solve_kernel(const double* __restrict__ mom, int groups, int n, int classes, double ridge,
-                 ut_cva_out out) {
+                 int want, ut_cva_out out) {
   __shared__ Smem s;
   const int tid = threadIdx.x;
   const int i = tid / N, j = tid % N;
@@ -387,6 +496,12 @@ cva_solve_kernel(const double* __restrict__ mom, int groups, int n, int classes,
     s.m[i * LD + j] = w;
     s.a[i * LD + j] = b;
   }
+  // H = [sqrt(n_c) (m_c - m)] for the low-rank path
+  if (classes <= kMaxC && i < n && j < classes) {
+    const double cnt = out.counts[j];
+    s.h[i * LD + j] =
+        cnt > 0.0 ? sqrt(cnt) * (out.class_means[j * n + i] - out.grand_mean[i]) : 0.0;
+  }
   __syncthreads();
   // symmetrize both (projection.py:199-200) and publish the scatter pair
   double wsym = 0.0, bsym = 0.0;
@@ -402,7 +517,21 @@ cva_solve_kernel(const double* __restrict__ mom, int groups, int n, int classes,
     out.between[i * n + j] = bsym;
   }
   __syncthreads();
-  const int code = solve_pair(s, n, true, ridge, out.evals, out.evecs, out.aux);
+  int live = 0;
+  for (int c = 0; c < classes; ++c) live += out.counts[c] > 0.0;
+  if (classes <= kMaxC && classes <= n && want >= 1 && want <= live - 1) {
+    if (cva_low_rank(s, n, classes, ridge, want, out)) {
+      if (tid == 0) *out.info = 0;
+      return;
+    }
+    __syncthreads();  // fall back: restore W and S_b
+    if (i < n && j < n) {
+      s.m[i * LD + j] = out.within[i * n + j];
+      s.a[i * LD + j] = out.between[i * n + j];
+    }
+    __syncthreads();
+  }
+  const int code = solve_full(s, n, true, ridge, false, out.evals, out.evecs, out.aux);
   if (tid == 0) *out.info = code;
 }
 
@@ -416,10 +545,10 @@ pca_solve_kernel(const double* __restrict__ mom, int groups, int n, ut_pca_out o
   if (tid == 0) {
     double tot = 0.0;
     for (int g = 0; g < groups; ++g) tot += mom[(size_t)g * len];
-    s.scal[2] = tot;
+    s.scal[3] = tot;
   }
   __syncthreads();
-  const double tot = s.scal[2];
+  const double tot = s.scal[3];
   if (tid < n) {
     double mean;
     if (groups == 1) {
@@ -454,14 +583,11 @@ pca_solve_kernel(const double* __restrict__ mom, int groups, int n, ut_pca_out o
     s.v[tid] = sd;
   }
   __syncthreads();
-  if (i < n && j < n) {
-    const double c = s.x[i * LD + j] / (tot - 1.0) / (s.v[i] * s.v[j]);
-    s.a[i * LD + j] = c;
-  }
+  if (i < n && j < n) s.a[i * LD + j] = s.x[i * LD + j] / (tot - 1.0) / (s.v[i] * s.v[j]);
   __syncthreads();
   if (i < n && j < n) out.corr[i * n + j] = 0.5 * (s.a[i * LD + j] + s.a[j * LD + i]);
   __syncthreads();
-  const int code = solve_pair(s, n, false, 0.0, out.evals, out.evecs, nullptr);
+  const int code = solve_full(s, n, false, 0.0, false, out.evals, out.evecs, nullptr);
   if (tid == 0) *out.info = code;
 }
 
@@ -476,19 +602,19 @@ int ut_gen_eig_sym(const double* A, const double* M, int32_t bands, double ridge
                    double* evecs, double* aux, int32_t* info, void* stream) {
   UT_REQUIRE(bands >= 1 && bands <= kMaxBands, "ut_gen_eig_sym: size must be 1..32");
   UT_REQUIRE(!M || aux, "ut_gen_eig_sym: aux required for the generalized problem");
-  gen_eig_kernel<<<1, kThreads, 0, as_stream(stream)>>>(A, M, bands, ridge, evals, evecs,
-                                                            aux, info);
+  gen_eig_kernel<<<1, kThreads, 0, as_stream(stream)>>>(A, M, bands, ridge, evals, evecs, aux,
+                                                        info);
   UT_CHECK_LAUNCH("gen_eig_kernel");
   return UT_OK;
 }
 
 int ut_cva_solve(const double* moments, int32_t groups, int32_t bands, int32_t classes,
-                 double ridge, const ut_cva_out* out, void* stream) {
+                 double ridge, int32_t want, const ut_cva_out* out, void* stream) {
   UT_REQUIRE(bands >= 1 && bands <= kMaxBands, "ut_cva_solve: bands must be 1..32");
   UT_REQUIRE(groups >= 1 && classes >= 1, "ut_cva_solve: bad groups/classes");
   UT_REQUIRE(out, "ut_cva_solve: null output");
-  cva_solve_kernel<<<1, kThreads, 0, as_stream(stream)>>>(moments, groups, bands, classes,
-                                                              ridge, *out);
+  cva_solve_kernel<<<1, kThreads, 0, as_stream(stream)>>>(moments, groups, bands, classes, ridge,
+                                                          want, *out);
   UT_CHECK_LAUNCH("cva_solve_kernel");
   return UT_OK;
 }

@@ -356,23 +356,41 @@ stretch_kernel(const float* __restrict__ scores, const float* __restrict__ minma
   using Code = typename std::conditional<DEPTH == 8, uint8_t, uint16_t>::type;
   constexpr double top = DEPTH == 8 ? 255.0 : 65535.0;
   __shared__ double lo_s[kMaxBands], sc_s[kMaxBands];
+  __shared__ float lof_s[kMaxBands], scf_s[kMaxBands];
   __shared__ int flat_s[kMaxBands];
   for (int c = threadIdx.x; c < k; c += blockDim.x) {
     const double lo = -(double)minmax[c], hi = (double)minmax[ld_mm + c];
     lo_s[c] = lo;
     flat_s[c] = (lo == hi) || !(lo < hi);  // constant plane (rendering.py:128-129)
     sc_s[c] = flat_s[c] ? 0.0 : top / (hi - lo);
+    lof_s[c] = (float)lo;
+    scf_s[c] = (float)sc_s[c];
   }
   __syncthreads();
   Code* codes = static_cast<Code*>(codes_raw);
   const int64_t total = (int64_t)k * npix;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  auto code_of = [&](float v, int c) -> Code {
-    if (flat_s[c]) return (Code)0;
+  // Exact reference arithmetic in fp64.  For 8-bit codes an fp32 evaluation
+  // is used first: its error is < 1e-4 code units (|x| <= 255.5), so unless the
+  // value lands within 2e-4 of a rounding boundary the fp32 code is the fp64
+  // code; the rare boundary cases are recomputed in fp64 (bit-exact result).
+  auto code_exact = [&](float v, int c) -> Code {
     double x = ((double)v - lo_s[c]) * sc_s[c];
     x = fmin(fmax(x, 0.0), top);
     return (Code)(int)floor(x + 0.5);
+  };
+  auto code_of = [&](float v, int c) -> Code {
+    if (flat_s[c]) return (Code)0;
+    if constexpr (DEPTH == 8) {
+      float x = (v - lof_s[c]) * scf_s[c];
+      x = fminf(fmaxf(x, 0.0f), 255.0f);
+      const float y = x + 0.5f;
+      const float fl = floorf(y);
+      const float fr = y - fl;
+      if (fr > 2e-4f && fr < 1.0f - 2e-4f) return (Code)(int)fl;
+    }
+    return code_exact(v, c);
   };
   if (vec16) {
     // 16 consecutive scores of one plane per thread (npix % 16 == 0)

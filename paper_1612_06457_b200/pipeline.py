@@ -24,7 +24,7 @@ import torch.distributed as dist
 
 from . import _lib
 from . import device as dev
-from .annotations import check_points, gather
+from .annotations import check_points
 from .eigen import DEFAULT_RIDGE, raise_for_info
 from .errors import DataError
 from .projection import (CvaDevice, PcaDevice, ProjectionModel, METHOD_CVA,
@@ -87,7 +87,7 @@ class CvaPipeline(_Sharded):
             self.xy = dev.to_device(xy, self.device)
             self.cls = dev.to_device(cls[own] if self.n else np.zeros(1, np.int32), self.device)
             self.fit = CvaDevice(b, len(self.class_ids), self.device, groups=self.world)
-            self.values = torch.empty((b, max(self.n, 1)), dtype=torch.float64, device=self.device)
+            self.cube = stack.cube()
             self.first_bad = torch.full((1,), -1, dtype=torch.int64, device=self.device)
             self.scores = torch.empty((self.k, stack.height, stack.width), dtype=torch.float32,
                                       device=self.device)
@@ -101,14 +101,9 @@ class CvaPipeline(_Sharded):
 
     # -- the hot path -------------------------------------------------------
     def fit_only(self):
-        L = _lib.lib()
-        if self.n:
-            _lib.check(L.ut_gather(self.ds.cube(), self.xy.data_ptr(), self.n,
-                                   self.values.data_ptr(), self.values.shape[1],
-                                   self.first_bad.data_ptr(), dev.stream_handle()), "ut_gather")
-        self.fit.moments_from(self.values, self.values.shape[1], self.cls, self.n)
+        self.fit.moments_from_cube(self.cube, self.xy, self.cls, self.n, self.first_bad)
         self.gather_moments(self.fit)
-        self.fit.solve(self.ridge)
+        self.fit.solve(self.ridge, self.k)
 
     def project_kernel(self):
         project_device(self.ds, self.evecs, self.mean, None, range(self.k), self.precision,
@@ -146,8 +141,8 @@ class CvaPipeline(_Sharded):
                                eigenvalues=np.ascontiguousarray(h["evals"][:self.k]))
 
     def launches(self) -> int:
-        """Our kernels per run(): gather, 2x moments, solve, K4 groups, stretch."""
-        return (1 if self.n else 0) + (2 if self.n else 0) + 1 + (self.k + 7) // 8 + 1
+        """Our kernels per run(): moments + merge, solve, K4 groups, stretch."""
+        return (2 if self.n else 0) + 1 + (self.k + 7) // 8 + 1
 
 
 class PcaPipeline(_Sharded):

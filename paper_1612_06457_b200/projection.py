@@ -194,10 +194,25 @@ class CvaDevice:
                                       self.moments.data_ptr(), ws.data_ptr(), ws.numel(),
                                       dev.stream_handle()), "ut_class_moments")
 
-    def solve(self, ridge: float):
+    def moments_from_cube(self, cube, xy_d: torch.Tensor, cls_d: torch.Tensor, n: int,
+                          first_bad: torch.Tensor):
+        """Fused K1: gather the n training pixels from the cube + class moments."""
+        L = _lib.lib()
+        if n == 0:
+            self.local_moments().zero_()
+            return
+        ws = dev.workspace("class_moments", L.ut_class_moments_ws(n, self.b, self.c),
+                           xy_d.device)
+        _lib.check(L.ut_cube_class_moments(C.byref(cube), xy_d.data_ptr(), cls_d.data_ptr(), n,
+                                           self.c, self.moments.data_ptr(), first_bad.data_ptr(),
+                                           ws.data_ptr(), ws.numel(), dev.stream_handle()),
+                   "ut_cube_class_moments")
+
+    def solve(self, ridge: float, want: int = 0):
+        """K3; ``want`` leading eigenvectors (0 = all B)."""
         _lib.check(_lib.lib().ut_cva_solve(self.moments.data_ptr(), self.groups, self.b, self.c,
-                                           float(ridge), C.byref(self.out), dev.stream_handle()),
-                   "ut_cva_solve")
+                                           float(ridge), int(want), C.byref(self.out),
+                                           dev.stream_handle()), "ut_cva_solve")
 
     def host(self) -> dict:
         flat = self.flat.cpu().numpy()
@@ -226,7 +241,7 @@ def _design_on_device(dm: DesignMatrix, device):
     return v, v.shape[1]
 
 
-def _scatter_device(dm: DesignMatrix, ridge: float):
+def _scatter_device(dm: DesignMatrix, ridge: float, want: int = 0):
     ids, cls = class_index(dm.labels)
     if len(ids) < 2:
         raise DataError(f"scatter needs at least 2 classes with points, got {len(ids)}")
@@ -238,13 +253,13 @@ def _scatter_device(dm: DesignMatrix, ridge: float):
         cls_d = dev.to_device(cls, device)
         fit = CvaDevice(dm.band_count, len(ids), device)
         fit.moments_from(values, ld, cls_d, dm.point_count)
-        fit.solve(ridge)
+        fit.solve(ridge, want)
         return ids, fit.host()
 
 
 def compute_scatter(dm: DesignMatrix) -> ScatterPair:
     """Pooled within/between-class scatter, symmetrized (projection.py:172-201)."""
-    ids, h = _scatter_device(dm, DEFAULT_RIDGE)
+    ids, h = _scatter_device(dm, DEFAULT_RIDGE, want=1)
     return ScatterPair(h["within"], h["between"], h["class_means"], ids,
                        h["counts"].astype(np.intp), h["grand_mean"])
 
@@ -264,9 +279,9 @@ def _training_scores(dm: DesignMatrix, coeffs: np.ndarray, mean: np.ndarray):
 def fit_cva(dm: DesignMatrix, k: int | None = None, ridge: float = DEFAULT_RIDGE,
             provenance: dict | None = None) -> ProjectionModel:
     """Canonical variates on raw values (projection.py:211-237)."""
-    ids, h = _scatter_device(dm, ridge)
-    raise_for_info(h["info"], h["aux"])
     k = _top_k(k, dm.band_count)
+    ids, h = _scatter_device(dm, ridge, want=k)
+    raise_for_info(h["info"], h["aux"])
     coeffs = np.ascontiguousarray(h["evecs"][:, :k])
     mean = h["grand_mean"]
     return ProjectionModel(method=METHOD_CVA, mean=mean, std=None, coefficients=coeffs,

@@ -451,7 +451,9 @@ def test_cfg3_full_size_properties():
     sample = host_rows(stack.planes)
     design = np.stack([stack.planes[:, int(y), int(x)].cpu().numpy()
                        for x, y in zip(scene.xs[:50], scene.ys[:50])], axis=1)
-    assert np.array_equal(design, pipe.values[:, :50].cpu().numpy())
+    xy = torch.from_numpy(np.stack([scene.xs[:50], scene.ys[:50]], 1).astype(np.int32)).cuda()
+    gathered, bad = ut.annotations.gather(stack, xy, 50)
+    assert np.array_equal(design, gathered.cpu().numpy()) and int(bad.item()) == -1
     ref_scores = oracle.project(sample, {"mean": model.mean, "std": None,
                                          "coefficients": model.coefficients})
     dev_scores = host_rows(pipe.scores).astype(np.float64)
@@ -464,3 +466,29 @@ def test_cfg3_full_size_properties():
         want = oracle.linear_to_codes(dev_scores[j], lo, hi)
         assert np.array_equal(dev_codes[j], want)
         assert int(codes[j].min()) == 0 and int(codes[j].max()) == 255
+
+
+def test_stretch_ties_and_boundaries_bit_exact():
+    """K5's fp32 fast path must reproduce the reference fp64 rounding exactly,
+    including ties (x.5 -> away from zero) and values next to them."""
+    from paper_1612_06457_b200.rendering import stretch_planes
+
+    rng = np.random.default_rng(7)
+    ties = np.arange(0.0, 255.0, 0.5, dtype=np.float32)
+    near = np.nextafter(ties, np.float32(np.inf)).astype(np.float32)
+    below = np.nextafter(ties, np.float32(-np.inf)).astype(np.float32)
+    rand = rng.uniform(-3, 300, size=4096).astype(np.float32)
+    vals = np.concatenate([ties, near, below, rand, [np.float32(0), np.float32(255)]])
+    pad = (-len(vals)) % 16
+    vals = np.concatenate([vals, np.full(pad, 17.25, np.float32)])
+    for lo, hi in ((0.0, 255.0), (-3.0, 300.0), (1.5, 2.75)):
+        plane = np.clip(vals, lo, hi).astype(np.float32)
+        lo32, hi32 = float(plane.min()), float(plane.max())
+        scores = torch.from_numpy(plane.reshape(1, 1, -1)).cuda()
+        mm = torch.tensor([-lo32, hi32], dtype=torch.float32, device="cuda")
+        got = stretch_planes(scores, mm).cpu().numpy().reshape(-1)
+        want = oracle.linear_to_codes(plane.astype(np.float64), lo32, hi32)
+        assert np.array_equal(got, want), (lo, hi)
+        got16 = stretch_planes(scores, mm, depth=16).cpu().numpy().reshape(-1)
+        want16 = oracle.linear_to_codes(plane.astype(np.float64), lo32, hi32, 16)
+        assert np.array_equal(got16, want16), (lo, hi)
