@@ -393,28 +393,38 @@ stretch_kernel(const float* __restrict__ scores, const float* __restrict__ minma
     return code_exact(v, c);
   };
   if (vec16) {
-    // 16 consecutive scores of one plane per thread (npix % 16 == 0)
-    const int64_t chunks = total / 16;
-    for (int64_t q = tid; q < chunks; q += stride) {
-      const int64_t e0 = q * 16;
-      const int c = (int)(e0 / npix);
-      float v[16];
+    // plane c = blockIdx.y; 16 consecutive scores per thread per step, two
+    // steps' loads issued together (npix % 16 == 0)
+    const int c = blockIdx.y;
+    const float* src = scores + (int64_t)c * npix;
+    Code* dst = codes + (int64_t)c * npix;
+    const int64_t chunks = npix / 16;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < chunks; q += 2 * step) {
+      float v[2][16];
+      const bool two = q + step < chunks;
 #pragma unroll
-      for (int i = 0; i < 16; i += 4) {
-        const uint4 u = ld_stream_u4(scores + e0 + i);
-        v[i] = __uint_as_float(u.x);
-        v[i + 1] = __uint_as_float(u.y);
-        v[i + 2] = __uint_as_float(u.z);
-        v[i + 3] = __uint_as_float(u.w);
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && !two) break;
+        const float* p = src + (q + h * step) * 16;
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+          const uint4 u = ld_stream_u4(p + i);
+          v[h][i] = __uint_as_float(u.x);
+          v[h][i + 1] = __uint_as_float(u.y);
+          v[h][i + 2] = __uint_as_float(u.z);
+          v[h][i + 3] = __uint_as_float(u.w);
+        }
       }
-      Code out[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) out[i] = code_of(v[i], c);
-      if constexpr (DEPTH == 8) {
-        st_stream_u4(codes + e0, *reinterpret_cast<const uint4*>(out));
-      } else {
-        st_stream_u4(codes + e0, *reinterpret_cast<const uint4*>(out));
-        st_stream_u4(codes + e0 + 8, *reinterpret_cast<const uint4*>(out + 8));
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && !two) break;
+        Code out[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) out[i] = code_of(v[h][i], c);
+        Code* o = dst + (q + h * step) * 16;
+        st_stream_u4(o, *reinterpret_cast<const uint4*>(out));
+        if constexpr (DEPTH == 16) st_stream_u4(o + 8, *reinterpret_cast<const uint4*>(out + 8));
       }
     }
   } else {
@@ -489,15 +499,22 @@ int ut_stretch(const float* scores, const float* minmax, int32_t k, int32_t ld_m
   cudaStream_t st = as_stream(stream);
   const bool vec16 = (npix % 16 == 0) && (reinterpret_cast<uintptr_t>(scores) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(codes) % 16 == 0);
-  const int64_t units = vec16 ? (int64_t)k * npix / 16 : (int64_t)k * npix;
-  int64_t grid = (units + kThreads - 1) / kThreads;
-  const int64_t cap = (int64_t)sm_count() * 8;
-  if (grid > cap) grid = cap;
-  if (grid < 1) grid = 1;
+  dim3 grid;
+  if (vec16) {
+    const int64_t chunks = npix / 16;
+    int64_t gx = (chunks + 2 * kThreads - 1) / (2 * kThreads);
+    int64_t cap = ((int64_t)sm_count() * 8 + k - 1) / k;
+    if (gx > cap) gx = cap;
+    grid = dim3((unsigned)(gx < 1 ? 1 : gx), (unsigned)k);
+  } else {
+    int64_t g = ((int64_t)k * npix + kThreads - 1) / kThreads;
+    const int64_t cap = (int64_t)sm_count() * 8;
+    grid = dim3((unsigned)(g > cap ? cap : (g < 1 ? 1 : g)));
+  }
   if (depth == 8)
-    stretch_kernel<8><<<(int)grid, kThreads, 0, st>>>(scores, minmax, k, ld_minmax, npix, codes, vec16);
+    stretch_kernel<8><<<grid, kThreads, 0, st>>>(scores, minmax, k, ld_minmax, npix, codes, vec16);
   else
-    stretch_kernel<16><<<(int)grid, kThreads, 0, st>>>(scores, minmax, k, ld_minmax, npix, codes, vec16);
+    stretch_kernel<16><<<grid, kThreads, 0, st>>>(scores, minmax, k, ld_minmax, npix, codes, vec16);
   UT_CHECK_LAUNCH("stretch_kernel");
   return UT_OK;
 }

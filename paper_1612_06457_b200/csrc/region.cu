@@ -3,14 +3,19 @@
 // Reference: fit_pca_unsupervised (projection.py:298-347) reads the cube twice
 // -- a per-band mean pass (:327-329) and a 64-row centred Gram pass
 // (:330-334).  Here one pass accumulates, per pixel, d = x - s with s a fixed
-// per-band shift (mean of a deterministic strided sample, so |mean - s| is
-// tiny and the one-pass form M2 = sum d d^T - (sum d)(sum d)^T / n loses
-// nothing at the 1e-9 bar; SURVEY Appendix B.7 measured <= 5e-15).
+// per-band shift (mean of a deterministic strided sample of 4096 pixels, so
+// |mean - s| ~ sigma/64 and the one-pass form M2 = sum d d^T - (sum d)(sum d)^T/n
+// loses nothing at the 1e-9 bar; SURVEY Appendix B.7 measured <= 5e-15).
 //
-// Tiles of 64 pixels are staged in shared memory as fp64 deviations; the Gram
-// upper triangle is split in 4x4 register blocks, several thread groups per
-// block striding over the tile's pixels.  This is fp64-issue-bound for B = 32
-// (528 DFMA per pixel), HBM-bound for B <= 16.  All reductions are fixed-order.
+// G = min(tiles, 592) CTAs (a constant, so results do not depend on the GPU)
+// each own a contiguous run of 64-pixel tiles.  A tile is staged in shared
+// memory as fp64 deviations with a constant-1 column appended (so the Gram
+// also yields the sums); the next tile is prefetched into registers while the
+// current one is reduced.  The upper triangle of the Gram is split into 4x4
+// register blocks, several thread groups per block striding over the tile's
+// pixels.  fp64-FMA-bound for B = 32 (561 DFMA per pixel), HBM-bound for
+// B <= 16.  Partials are summed by a separate kernel, one warp per entry,
+// lanes over CTAs, in a fixed shuffle tree: deterministic.
 #include "common.cuh"
 
 namespace ut {
@@ -19,25 +24,24 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kTile = 64;
 constexpr int kSample = 4096;
-constexpr int kMaxGrid = 2048;
-constexpr int kBp = kMaxBands;                 // padded band count (multiple of 4)
-constexpr int kLdd = kBp + 1;                  // tile row stride (doubles)
-constexpr int kMaxBlk = (kBp / 4) * (kBp / 4 + 1) / 2;  // 36
-constexpr int kRec = kMaxBands + kMaxBands * kMaxBands;   // per-CTA partial: sum d, G
+constexpr int kMaxG = 592;                                  // 4 x 148
+constexpr int kCols = kMaxBands + 4;                        // bands + ones, padded to 4
+constexpr int kLdd = kCols + 1;                             // tile row stride (doubles)
+constexpr int kNb = kCols / 4;                              // 9 blocks per dim
+constexpr int kMaxBlk = kNb * (kNb + 1) / 2;                // 45
+constexpr int kEnt = kCols * kCols;                         // per-CTA Gram record (padded)
 
 struct RegionWs {
-  unsigned int* counter;
   double* shift;   // B
-  double* part;    // [grid][kRec]
+  double* part;    // [kEnt][G]
 };
 
 size_t region_ws_layout(RegionWs* ws, void* base) {
   const size_t off_shift = 256;
   const size_t off_part = off_shift + sizeof(double) * kMaxBands;
-  const size_t total = off_part + sizeof(double) * (size_t)kMaxGrid * kRec;
+  const size_t total = off_part + sizeof(double) * (size_t)kMaxG * kEnt;
   if (ws && base) {
     char* p = static_cast<char*>(base);
-    ws->counter = reinterpret_cast<unsigned int*>(p);
     ws->shift = reinterpret_cast<double*>(p + off_shift);
     ws->part = reinterpret_cast<double*>(p + off_part);
   }
@@ -51,49 +55,58 @@ struct Region {
   uint32_t w;
   int64_t npix;
   int bands;
+  int G;
+  int64_t tiles_per_cta;
 };
 
 template <typename T>
-__device__ __forceinline__ double sample_at(const Region& r, int b, int64_t pix) {
-  const int64_t y = pix / r.w, x = pix - y * r.w;
-  const T* p = static_cast<const T*>(r.data) + b * r.bs + (r.y0 + y) * r.rs + r.x0 + x;
-  return to_f64(*p);
+__device__ __forceinline__ const T* pixel_ptr(const Region& r, int64_t pix) {
+  const int64_t y = (int64_t)((uint64_t)pix / r.w), x = pix - y * r.w;
+  return static_cast<const T*>(r.data) + (r.y0 + y) * r.rs + r.x0 + x;
 }
 
-// shift_b = mean of up to 4096 pixels at a fixed stride (one CTA, fixed order)
+// shift_b = mean of up to 4096 pixels at a fixed stride (one CTA, fixed tree)
 template <typename T>
-__global__ void __launch_bounds__(kThreads) shift_kernel(Region r, RegionWs ws) {
-  __shared__ double red[kThreads];
+__global__ void __launch_bounds__(1024) shift_kernel(Region r, RegionWs ws) {
+  __shared__ double red[1024 / 32][kMaxBands];
   const int64_t count = r.npix < kSample ? r.npix : kSample;
   const int64_t step = r.npix / count;
-  for (int b = 0; b < r.bands; ++b) {
-    double acc = 0.0;
-    for (int64_t i = threadIdx.x; i < count; i += blockDim.x) acc += sample_at<T>(r, b, i * step);
-    red[threadIdx.x] = acc;
-    __syncthreads();
-    for (int h = kThreads / 2; h > 0; h >>= 1) {
-      if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) ws.shift[b] = red[0] / (double)count;
-    __syncthreads();
+  double acc[kMaxBands];
+#pragma unroll
+  for (int b = 0; b < kMaxBands; ++b) acc[b] = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) {
+    const T* p = pixel_ptr<T>(r, i * step);
+#pragma unroll
+    for (int b = 0; b < kMaxBands; ++b)
+      if (b < r.bands) acc[b] += to_f64(p[b * r.bs]);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int b = 0; b < kMaxBands; ++b) {
+    double v = acc[b];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][b] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < r.bands) {
+    double v = 0.0;
+    for (int w = 0; w < 32; ++w) v += red[w][threadIdx.x];
+    ws.shift[threadIdx.x] = v / (double)count;
   }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
-region_kernel(Region r, RegionWs ws, double* __restrict__ moments) {
+region_kernel(Region r, RegionWs ws) {
   __shared__ double tile[kTile * kLdd];
   __shared__ double shift[kMaxBands];
-  __shared__ double gsum[kThreads / 32];
   const int tid = threadIdx.x;
   const int B = r.bands;
-  const int nb = (B + 3) / 4;                     // 4-band blocks per dim
+  const int nb = (B + 1 + 3) / 4;                 // 4-column blocks incl. the ones column
   const int nblk = nb * (nb + 1) / 2;
-  const int groups = kThreads / nblk;             // pixel-stride groups
+  const int groups = kThreads / nblk;
   const int blk = tid % nblk, grp = tid / nblk;
   const bool gram_thread = grp < groups;
-  // (bi, bj) of this thread's 4x4 block, bi <= bj
   int bi = 0, bj = 0;
   {
     int rem = blk;
@@ -109,28 +122,36 @@ region_kernel(Region r, RegionWs ws, double* __restrict__ moments) {
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
-  double dsum = 0.0;  // sum of deviations of band `tid` (tid < B)
 
   const int64_t ntiles = (r.npix + kTile - 1) / kTile;
-  const int p_own = tid % kTile;        // staging: fixed pixel per thread
-  const int b_first = tid / kTile;      // and bands b_first, b_first + 4, ...
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  const int64_t t0 = (int64_t)blockIdx.x * r.tiles_per_cta;
+  int64_t t1 = t0 + r.tiles_per_cta;
+  if (t1 > ntiles) t1 = ntiles;
+  const int p_own = tid % kTile;      // staging: one pixel per thread
+  const int b_first = tid / kTile;    // bands b_first, +4, +8, ...
+  constexpr int kPer = (kMaxBands + 3) / 4;  // <= 8 staged values per thread
+  double next[kPer];
+  bool next_valid = false;
+  auto load = [&](int64_t t) {
     const int64_t pix = t * kTile + p_own;
-    const bool valid = pix < r.npix;
-    int64_t base = 0;
-    if (valid) {
-      const int64_t y = (int64_t)((uint64_t)pix / r.w), x = pix - y * r.w;
-      base = (r.y0 + y) * r.rs + r.x0 + x;
+    next_valid = pix < r.npix;
+    const T* src = next_valid ? pixel_ptr<T>(r, pix) : nullptr;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int b = b_first + 4 * u;
+      next[u] = (next_valid && b < B) ? to_f64(src[b * r.bs]) : 0.0;
     }
-    const T* src = static_cast<const T*>(r.data) + base;
-    for (int b = b_first; b < B; b += kThreads / kTile)
-      tile[p_own * kLdd + b] = valid ? to_f64(src[b * r.bs]) - shift[b] : 0.0;
+  };
+  if (t0 < t1) load(t0);
+  for (int64_t t = t0; t < t1; ++t) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int b = b_first + 4 * u;
+      if (b < B) tile[p_own * kLdd + b] = next_valid ? next[u] - shift[b] : 0.0;
+    }
+    if (b_first == 0) tile[p_own * kLdd + B] = next_valid ? 1.0 : 0.0;
     __syncthreads();
-    if (tid < B) {
-      double s = 0.0;
-      for (int p = 0; p < kTile; ++p) s += tile[p * kLdd + tid];
-      dsum += s;
-    }
+    if (t + 1 < t1) load(t + 1);      // prefetch while this tile is reduced
     if (gram_thread) {
       for (int p = grp; p < kTile; p += groups) {
         const double* row = tile + p * kLdd;
@@ -148,76 +169,70 @@ region_kernel(Region r, RegionWs ws, double* __restrict__ moments) {
     }
     __syncthreads();
   }
-
-  // ---- CTA reduction of the thread-group partials (fixed order over groups)
-  double* red = tile;  // reuse: needs nblk*16*groups <= kTile*kLdd doubles? use two phases
-  double* part = ws.part + (size_t)blockIdx.x * kRec;
-  if (tid < B) part[tid] = dsum;
+  // reduce the thread groups (fixed order) and write this CTA's partial
+  double* red = tile;  // nblk * 16 <= 720 doubles <= kTile * kLdd
   for (int g = 0; g < groups; ++g) {
     if (gram_thread && grp == g) {
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) red[blk * 16 + a * 4 + c] = (g == 0 ? 0.0 : red[blk * 16 + a * 4 + c]) + acc[a][c];
+        for (int c = 0; c < 4; ++c) {
+          const int e = blk * 16 + a * 4 + c;
+          red[e] = (g == 0 ? 0.0 : red[e]) + acc[a][c];
+        }
     }
     __syncthreads();
   }
   for (int e = tid; e < nblk * 16; e += blockDim.x) {
-    int b2 = e / 16, a = (e % 16) / 4, c = e % 4;
+    const int b2 = e / 16, a = (e % 16) / 4, c = e % 4;
     int i0 = 0, rem = b2;
     while (rem >= nb - i0) { rem -= nb - i0; ++i0; }
     const int j0 = i0 + rem;
     const int i = 4 * i0 + a, j = 4 * j0 + c;
-    if (i < B && j < B) part[kMaxBands + i * kMaxBands + j] = red[e];
-  }
-  (void)gsum;
-  if (last_block_ticket(ws.counter)) {
-    // fixed-order sum over CTAs, then n, mean, M2 (full symmetric)
-    const double n = (double)r.npix;
-    for (int e = tid; e < kRec; e += blockDim.x) {
-      bool used;
-      if (e < kMaxBands) {
-        used = e < B;
-      } else {
-        const int q = e - kMaxBands, i = q / kMaxBands, j = q % kMaxBands;
-        used = i < B && j < B && (i / 4) <= (j / 4);
-      }
-      if (!used) continue;
-      double s = 0.0;
-      for (unsigned int g = 0; g < gridDim.x; ++g) s += ws.part[(size_t)g * kRec + e];
-      ws.part[e] = s;  // CTA 0's slot holds the totals (CTA 0 already wrote its own)
-    }
-    __syncthreads();
-    const int len = 1 + B + B * B;
-    if (tid == 0) moments[0] = n;
-    if (tid < B) moments[1 + tid] = shift[tid] + ws.part[tid] / n;
-    for (int e = tid; e < B * B; e += blockDim.x) {
-      const int i = e / B, j = e % B;
-      const int lo = (i / 4) <= (j / 4) ? i : j, hi = (i / 4) <= (j / 4) ? j : i;
-      const double g = ws.part[kMaxBands + lo * kMaxBands + hi];
-      moments[1 + B + e] = g - ws.part[i] * ws.part[j] / n;
-    }
-    (void)len;
-    if (tid == 0) *ws.counter = 0u;
+    ws.part[(size_t)(i * kCols + j) * r.G + blockIdx.x] = red[e];
   }
 }
 
-template <typename T>
-int launch_region(const Region& r, RegionWs ws, double* moments, cudaStream_t st) {
-  shift_kernel<T><<<1, kThreads, 0, st>>>(r, ws);
-  UT_CHECK_LAUNCH("shift_kernel");
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, region_kernel<T>, kThreads, 0);
-    per_sm = n > 0 ? n : 1;
+// moments = [n, mean, M2]; one warp per output entry, lanes over the G partials.
+__global__ void __launch_bounds__(256)
+region_merge_kernel(Region r, RegionWs ws, double* __restrict__ moments) {
+  const int B = r.bands, G = r.G;
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int total = 1 + B + B * B;
+  if (e >= total) return;
+  auto entry = [&](int i, int j) {  // Gram entry (i <= j by block) summed over CTAs
+    if ((i >> 2) > (j >> 2)) { const int t = i; i = j; j = t; }
+    const double* p = ws.part + (size_t)(i * kCols + j) * G;
+    double a = 0.0;
+    for (int g = lane; g < G; g += 32) a += p[g];
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    return a;
+  };
+  const double n = (double)r.npix;
+  double v;
+  if (e == 0) {
+    v = n;
+  } else if (e <= B) {
+    const int b = e - 1;
+    v = ws.shift[b] + entry(b, B) / n;
+  } else {
+    const int q = e - 1 - B, i = q / B, j = q - i * B;
+    const double sij = entry(i, j), si = entry(i, B), sj = entry(j, B);
+    v = sij - si * sj / n;
   }
-  const int64_t ntiles = (r.npix + kTile - 1) / kTile;
-  int64_t grid = (int64_t)per_sm * sm_count();
-  if (grid > ntiles) grid = ntiles;
-  if (grid > kMaxGrid) grid = kMaxGrid;
-  region_kernel<T><<<(int)grid, kThreads, 0, st>>>(r, ws, moments);
+  if (lane == 0) moments[e] = v;
+}
+
+template <typename T>
+int launch_region(Region r, RegionWs ws, double* moments, cudaStream_t st) {
+  shift_kernel<T><<<1, 1024, 0, st>>>(r, ws);
+  UT_CHECK_LAUNCH("shift_kernel");
+  region_kernel<T><<<r.G, kThreads, 0, st>>>(r, ws);
   UT_CHECK_LAUNCH("region_kernel");
+  const int total = 1 + r.bands + r.bands * r.bands;
+  region_merge_kernel<<<(total + 7) / 8, 256, 0, st>>>(r, ws, moments);
+  UT_CHECK_LAUNCH("region_merge_kernel");
   return UT_OK;
 }
 
@@ -243,15 +258,24 @@ int ut_region_moments(const ut_cube* cube, int64_t x0, int64_t y0, int64_t w, in
              "region (%lld, %lld, %lld, %lld) outside %lldx%lld stack", (long long)x0,
              (long long)y0, (long long)w, (long long)h, (long long)cube->cols,
              (long long)cube->rows);
-  UT_REQUIRE(w * h < (int64_t)1 << 32, "region too large for 32-bit pixel indexing");
+  UT_REQUIRE(w * h < ((int64_t)1 << 40), "region too large");
   RegionWs ws;
   const size_t need = region_ws_layout(&ws, ws_base);
   UT_REQUIRE(ws_bytes >= need, "ut_region_moments: workspace %zu < %zu", ws_bytes, need);
+  Region r{};
+  r.data = cube->data;
+  r.bs = cube->band_stride;
+  r.rs = cube->row_stride;
+  r.x0 = x0;
+  r.y0 = y0;
+  r.w = (uint32_t)w;
+  r.npix = w * h;
+  r.bands = cube->bands;
+  const int64_t ntiles = (r.npix + kTile - 1) / kTile;
+  const int64_t G = ntiles < kMaxG ? ntiles : kMaxG;
+  r.tiles_per_cta = (ntiles + G - 1) / G;
+  r.G = (int)((ntiles + r.tiles_per_cta - 1) / r.tiles_per_cta);
   cudaStream_t st = as_stream(stream);
-  cudaError_t e = cudaMemsetAsync(ws.counter, 0, sizeof(unsigned int), st);
-  if (e != cudaSuccess) return cuda_status(e, "ut_region_moments memset");
-  Region r{cube->data, cube->band_stride, cube->row_stride, x0, y0, (uint32_t)w, w * h,
-           cube->bands};
   switch (cube->dtype) {
     case UT_U8: return launch_region<uint8_t>(r, ws, moments, st);
     case UT_U16: return launch_region<uint16_t>(r, ws, moments, st);
