@@ -16,6 +16,8 @@
 //
 // K5 re-reads the fp32 planes and applies the reference's arithmetic exactly
 // in fp64: code = floor(clip((v - lo) * (top / (hi - lo)), 0, top) + 0.5).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ut {
@@ -104,6 +106,7 @@ template <typename T, int VEC, int KG, bool F64>
 struct Proj {
   using Acc = typename std::conditional<F64, double, float>::type;
   static constexpr int LB = VEC * (int)sizeof(T);  // load bytes per band
+  static_assert(LB >= 1, "");
 
   // shared: weights [B][KG], shifts [B], bias [KG]
   struct Smem {
@@ -185,6 +188,42 @@ struct Proj {
     }
   }
 
+  // One VEC-pixel group read from a shared-memory stage [bands][P] (TMA path).
+  __device__ static void group_smem(const ProjParams& p, const Smem& s, const T* stage, int P,
+                                    int lp, int64_t base, float* mn, float* mx, float& chk) {
+    Acc acc[KG][VEC];
+#pragma unroll
+    for (int k = 0; k < KG; ++k)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[k][v] = s.bias[k];
+    using U = typename Ld<LB>::U;
+#pragma unroll 4
+    for (int b = 0; b < p.bands; ++b) {
+      const U raw = *reinterpret_cast<const U*>(stage + (size_t)b * P + lp);
+      const T* xs = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        Acc d;
+        if constexpr (F64) d = to_f64(xs[v]) - s.mean[b];
+        else d = centred_f32<T>(xs[v], s.hi[b], s.mean[b]);
+#pragma unroll
+        for (int k = 0; k < KG; ++k) acc[k][v] = fma(s.w[b][k], d, acc[k][v]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      float out[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        out[v] = (float)acc[k][v];
+        mn[k] = fminf(mn[k], out[v]);
+        mx[k] = fmaxf(mx[k], out[v]);
+        chk = nan_guard(chk, out[v]);
+      }
+      store_scores<VEC>(p.scores + (int64_t)(p.k0 + k) * p.npix + base, out);
+    }
+  }
+
   // One pixel with general strides (tails, views, misaligned inputs).
   __device__ static void pixel_any(const ProjParams& p, const Smem& s, int64_t pix, float* mn,
                                    float* mx, float& chk) {
@@ -233,7 +272,7 @@ struct Proj {
     if (threadIdx.x <= 2 * KG) {
       const int f = threadIdx.x;
       float r = s.red[0][f];
-      for (int w = 1; w < kThreads / 32; ++w)
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
         r = (f == 2 * KG) ? r + s.red[w][f] : fmaxf(r, s.red[w][f]);
       p.part[(int64_t)blockIdx.x * (2 * KG + 1) + f] = r;
     }
@@ -283,6 +322,129 @@ project_kernel(ProjParams p) {
   P::finish(p, s, mn, mx, chk);
 }
 
+// ---------------------------------------------------------------- K4 (TMA)
+// Warp-specialized, persistent: warp 4 streams [bands][P]-sample tiles of the
+// cube into a 3-stage shared-memory ring with bulk async copies (one per band
+// per tile, completing on a transaction-count mbarrier); warps 0-3 consume
+// them.  Decouples HBM latency from the FMA stream at one CTA per SM.
+constexpr int kTmaConsumers = 128;
+constexpr int kTmaThreads = kTmaConsumers + 32;
+constexpr int kTmaStages = 3;
+constexpr int kTmaStageBytes = 64 * 1024;
+
+struct TmaShape {
+  int P;       // pixels per tile
+  int R;       // VEC-groups per consumer thread per tile
+  size_t smem; // dynamic shared bytes
+};
+
+template <typename T, int VEC>
+TmaShape tma_shape(int bands) {
+  const int unit = kTmaConsumers * VEC;  // pixels when each consumer takes one group
+  int R = kTmaStageBytes / (unit * bands * (int)sizeof(T));
+  if (R < 1) R = 1;
+  if (R > 8) R = 8;
+  TmaShape sh;
+  sh.P = unit * R;
+  sh.R = R;
+  sh.smem = (size_t)kTmaStages * sh.P * bands * sizeof(T) + 2 * kTmaStages * sizeof(uint64_t) + 128;
+  return sh;
+}
+
+template <typename T, int VEC, int KG, bool F64>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+project_tma_kernel(ProjParams p, int P, int R) {
+  using Pj = Proj<T, VEC, KG, F64>;
+  __shared__ typename Pj::Smem s;
+  extern __shared__ __align__(128) unsigned char dyn[];
+  const int B = p.bands;
+  T* stages = reinterpret_cast<T*>(dyn);
+  uint64_t* full = reinterpret_cast<uint64_t*>(dyn + (size_t)kTmaStages * P * B * sizeof(T));
+  uint64_t* empty = full + kTmaStages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < kTmaStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kTmaConsumers / 32);
+    }
+    mbar_fence_init();
+  }
+  Pj::setup(p, s);  // contains __syncthreads (all 160 threads)
+  float mn[KG], mx[KG], chk = 0.0f;
+#pragma unroll
+  for (int k = 0; k < KG; ++k) {
+    mn[k] = INFINITY;
+    mx[k] = -INFINITY;
+  }
+  const int64_t ntiles = (p.npix + P - 1) / P;
+  if (warp == kTmaConsumers / 32) {
+    // producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int i = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int st = i % kTmaStages;
+        const uint32_t ph = (uint32_t)(i / kTmaStages) & 1u;
+        if (i >= kTmaStages) mbar_wait(&empty[st], ph ^ 1u);
+        const int64_t p0 = t * P;
+        const int64_t npx = (p.npix - p0) < P ? (p.npix - p0) : P;
+        const uint32_t bytes = (uint32_t)(npx * sizeof(T));
+        mbar_expect_tx(&full[st], bytes * (uint32_t)B);
+        T* dst = stages + (size_t)st * P * B;
+        const T* src = static_cast<const T*>(p.data) + p0;
+        for (int b = 0; b < B; ++b)
+          bulk_g2s(dst + (size_t)b * P, src + (int64_t)b * p.bs, bytes, &full[st], pol);
+      }
+    }
+  } else {
+    int i = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int st = i % kTmaStages;
+      const uint32_t ph = (uint32_t)(i / kTmaStages) & 1u;
+      mbar_wait(&full[st], ph);
+      const int64_t p0 = t * P;
+      const int64_t npx = (p.npix - p0) < P ? (p.npix - p0) : P;
+      const T* stage = stages + (size_t)st * P * B;
+      for (int r = 0; r < R; ++r) {
+        const int lp = (r * kTmaConsumers + tid) * VEC;
+        if (lp + VEC <= npx) Pj::group_smem(p, s, stage, P, lp, p0 + lp, mn, mx, chk);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+  Pj::finish(p, s, mn, mx, chk);
+}
+
+bool tma_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("UT_PROJECT_TMA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <typename T, int VEC, int KG, bool F64>
+int launch_tma(ProjParams& p, cudaStream_t st) {
+  auto kern = project_tma_kernel<T, VEC, KG, F64>;
+  const TmaShape sh = tma_shape<T, VEC>(p.bands);
+  static size_t attr = 0;
+  if (attr < sh.smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sh.smem);
+    if (e != cudaSuccess) return cuda_status(e, "project_tma smem attribute");
+    attr = sh.smem;
+  }
+  const int64_t ntiles = (p.npix + sh.P - 1) / sh.P;
+  int64_t grid = sm_count();
+  if (grid > ntiles) grid = ntiles;
+  if (grid < 1) grid = 1;
+  kern<<<(int)grid, kTmaThreads, sh.smem, st>>>(p, sh.P, sh.R);
+  UT_CHECK_LAUNCH("project_tma_kernel");
+  return UT_OK;
+}
+
 template <typename T, int VEC, int KG, bool F64, bool VECTOR>
 int launch_one(ProjParams& p, cudaStream_t st) {
   auto kern = project_kernel<T, VEC, KG, F64, VECTOR>;
@@ -315,6 +477,13 @@ int launch_kg(ProjParams& p, bool vector_ok, cudaStream_t st) {
                        ((p.bs * (int64_t)sizeof(T)) % LB == 0) &&
                        (reinterpret_cast<uintptr_t>(p.scores) % 16 == 0) &&
                        (p.npix % 4 == 0);
+  // TMA path: every bulk copy 16-byte aligned (plane starts, tile starts, and
+  // the last partial tile); the npix % VEC tail would be skipped, so require 0.
+  const bool tma_ok = aligned && tma_enabled() && (p.npix % VEC == 0) &&
+                      ((p.npix * (int64_t)sizeof(T)) % 16 == 0) &&
+                      (reinterpret_cast<uintptr_t>(p.data) % 16 == 0) &&
+                      ((p.bs * (int64_t)sizeof(T)) % 16 == 0);
+  if (tma_ok) return launch_tma<T, VEC, KG, F64>(p, st);
   if (aligned) return launch_one<T, VEC, KG, F64, true>(p, st);
   return launch_one<T, 1, KG, F64, false>(p, st);
 }
@@ -371,31 +540,48 @@ stretch_kernel(const float* __restrict__ scores, const float* __restrict__ minma
   const int64_t total = (int64_t)k * npix;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  // Exact reference arithmetic in fp64.  For 8-bit codes an fp32 evaluation
-  // is used first: its error is < 1e-4 code units (|x| <= 255.5), so unless the
-  // value lands within 2e-4 of a rounding boundary the fp32 code is the fp64
-  // code; the rare boundary cases are recomputed in fp64 (bit-exact result).
-  auto code_exact = [&](float v, int c) -> Code {
-    double x = ((double)v - lo_s[c]) * sc_s[c];
+  // Exact reference arithmetic in fp64: floor(clip((v - lo) * s, 0, top) + 0.5).
+  // For 8-bit codes an fp32 evaluation is used first: its error is < 1e-4 code
+  // units (|x| <= 255.5), so unless x lies within 2e-4 of a tie (k + 0.5),
+  // round-to-nearest with saturation gives the same code; the rare near-tie
+  // values are recomputed in fp64, so the result is bit-exact.
+  struct Plane {
+    double lo, sc;
+    float lof, scf;
+    bool flat;
+  };
+  auto plane_of = [&](int c) {
+    Plane q;
+    q.lo = lo_s[c];
+    q.sc = sc_s[c];
+    q.lof = lof_s[c];
+    q.scf = scf_s[c];
+    q.flat = flat_s[c] != 0;
+    return q;
+  };
+  auto code_exact = [&](float v, const Plane& q) -> Code {
+    double x = ((double)v - q.lo) * q.sc;
     x = fmin(fmax(x, 0.0), top);
     return (Code)(int)floor(x + 0.5);
   };
-  auto code_of = [&](float v, int c) -> Code {
-    if (flat_s[c]) return (Code)0;
+  auto code_of = [&](float v, const Plane& q) -> Code {
+    if (q.flat) return (Code)0;
     if constexpr (DEPTH == 8) {
-      float x = (v - lof_s[c]) * scf_s[c];
-      x = fminf(fmaxf(x, 0.0f), 255.0f);
-      const float y = x + 0.5f;
-      const float fl = floorf(y);
-      const float fr = y - fl;
-      if (fr > 2e-4f && fr < 1.0f - 2e-4f) return (Code)(int)fl;
+      const float x = (v - q.lof) * q.scf;
+      const float r = rintf(x);
+      if (fabsf(x - r) < 0.5f - 2e-4f) {
+        unsigned short u;
+        asm("cvt.rni.sat.u8.f32 %0, %1;" : "=h"(u) : "f"(x));
+        return (Code)u;
+      }
     }
-    return code_exact(v, c);
+    return code_exact(v, q);
   };
   if (vec16) {
     // plane c = blockIdx.y; 16 consecutive scores per thread per step, two
     // steps' loads issued together (npix % 16 == 0)
     const int c = blockIdx.y;
+    const Plane pl = plane_of(c);
     const float* src = scores + (int64_t)c * npix;
     Code* dst = codes + (int64_t)c * npix;
     const int64_t chunks = npix / 16;
@@ -421,14 +607,15 @@ stretch_kernel(const float* __restrict__ scores, const float* __restrict__ minma
         if (h == 1 && !two) break;
         Code out[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) out[i] = code_of(v[h][i], c);
+        for (int i = 0; i < 16; ++i) out[i] = code_of(v[h][i], pl);
         Code* o = dst + (q + h * step) * 16;
         st_stream_u4(o, *reinterpret_cast<const uint4*>(out));
         if constexpr (DEPTH == 16) st_stream_u4(o + 8, *reinterpret_cast<const uint4*>(out + 8));
       }
     }
   } else {
-    for (int64_t e = tid; e < total; e += stride) codes[e] = code_of(scores[e], (int)(e / npix));
+    for (int64_t e = tid; e < total; e += stride)
+      codes[e] = code_of(scores[e], plane_of((int)(e / npix)));
   }
 }
 
