@@ -327,8 +327,6 @@ project_kernel(ProjParams p) {
 // cube into a 3-stage shared-memory ring with bulk async copies (one per band
 // per tile, completing on a transaction-count mbarrier); warps 0-3 consume
 // them.  Decouples HBM latency from the FMA stream at one CTA per SM.
-constexpr int kTmaConsumers = 128;
-constexpr int kTmaThreads = kTmaConsumers + 32;
 constexpr int kTmaStages = 3;
 constexpr int kTmaStageBytes = 64 * 1024;
 
@@ -338,9 +336,9 @@ struct TmaShape {
   size_t smem; // dynamic shared bytes
 };
 
-template <typename T, int VEC>
+template <typename T, int VEC, int CONS>
 TmaShape tma_shape(int bands) {
-  const int unit = kTmaConsumers * VEC;  // pixels when each consumer takes one group
+  const int unit = CONS * VEC;  // pixels when each consumer takes one group
   int R = kTmaStageBytes / (unit * bands * (int)sizeof(T));
   if (R < 1) R = 1;
   if (R > 8) R = 8;
@@ -351,8 +349,9 @@ TmaShape tma_shape(int bands) {
   return sh;
 }
 
-template <typename T, int VEC, int KG, bool F64>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+// CONS consumer threads + one producer warp.
+template <typename T, int VEC, int KG, bool F64, int CONS>
+__global__ void __launch_bounds__(CONS + 32, 1)
 project_tma_kernel(ProjParams p, int P, int R) {
   using Pj = Proj<T, VEC, KG, F64>;
   __shared__ typename Pj::Smem s;
@@ -365,11 +364,11 @@ project_tma_kernel(ProjParams p, int P, int R) {
   if (tid == 0) {
     for (int i = 0; i < kTmaStages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kTmaConsumers / 32);
+      mbar_init(&empty[i], CONS / 32);
     }
     mbar_fence_init();
   }
-  Pj::setup(p, s);  // contains __syncthreads (all 160 threads)
+  Pj::setup(p, s);  // contains __syncthreads (all threads)
   float mn[KG], mx[KG], chk = 0.0f;
 #pragma unroll
   for (int k = 0; k < KG; ++k) {
@@ -377,7 +376,7 @@ project_tma_kernel(ProjParams p, int P, int R) {
     mx[k] = -INFINITY;
   }
   const int64_t ntiles = (p.npix + P - 1) / P;
-  if (warp == kTmaConsumers / 32) {
+  if (warp == CONS / 32) {
     // producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
@@ -406,7 +405,7 @@ project_tma_kernel(ProjParams p, int P, int R) {
       const int64_t npx = (p.npix - p0) < P ? (p.npix - p0) : P;
       const T* stage = stages + (size_t)st * P * B;
       for (int r = 0; r < R; ++r) {
-        const int lp = (r * kTmaConsumers + tid) * VEC;
+        const int lp = (r * CONS + tid) * VEC;
         if (lp + VEC <= npx) Pj::group_smem(p, s, stage, P, lp, p0 + lp, mn, mx, chk);
       }
       __syncwarp();
@@ -425,10 +424,10 @@ bool tma_enabled() {
   return v == 1;
 }
 
-template <typename T, int VEC, int KG, bool F64>
+template <typename T, int VEC, int KG, bool F64, int CONS>
 int launch_tma(ProjParams& p, cudaStream_t st) {
-  auto kern = project_tma_kernel<T, VEC, KG, F64>;
-  const TmaShape sh = tma_shape<T, VEC>(p.bands);
+  auto kern = project_tma_kernel<T, VEC, KG, F64, CONS>;
+  const TmaShape sh = tma_shape<T, VEC, CONS>(p.bands);
   static size_t attr = 0;
   if (attr < sh.smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -440,7 +439,7 @@ int launch_tma(ProjParams& p, cudaStream_t st) {
   int64_t grid = sm_count();
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
-  kern<<<(int)grid, kTmaThreads, sh.smem, st>>>(p, sh.P, sh.R);
+  kern<<<(int)grid, CONS + 32, sh.smem, st>>>(p, sh.P, sh.R);
   UT_CHECK_LAUNCH("project_tma_kernel");
   return UT_OK;
 }
@@ -483,7 +482,16 @@ int launch_kg(ProjParams& p, bool vector_ok, cudaStream_t st) {
                       ((p.npix * (int64_t)sizeof(T)) % 16 == 0) &&
                       (reinterpret_cast<uintptr_t>(p.data) % 16 == 0) &&
                       ((p.bs * (int64_t)sizeof(T)) % 16 == 0);
-  if (tma_ok) return launch_tma<T, VEC, KG, F64>(p, st);
+  if (tma_ok) {
+    // fp64 accumulation is FMA-pipe heavy: 8 consumer warps, 2-4 pixels each;
+    // fp32: 4 consumer warps with 16-byte groups.
+    if constexpr (F64) {
+      constexpr int VT = (16 / (int)sizeof(T)) < 2 ? 1 : ((8 / (int)sizeof(T)) < 2 ? 2 : 8 / (int)sizeof(T));
+      if ((p.npix % VT) == 0) return launch_tma<T, VT, KG, F64, 256>(p, st);
+    } else {
+      return launch_tma<T, VEC, KG, F64, 128>(p, st);
+    }
+  }
   if (aligned) return launch_one<T, VEC, KG, F64, true>(p, st);
   return launch_one<T, 1, KG, F64, false>(p, st);
 }
