@@ -114,7 +114,7 @@ struct Proj {
     float hi[kMaxBands];
     double mean[kMaxBands];
     Acc bias[KG];
-    float red[kThreads / 32][2 * KG + 1];
+    float red[16][2 * KG + 1];  // up to 16 warps (TMA kernel: 9)
   };
 
   __device__ static void setup(const ProjParams& p, Smem& s) {
