@@ -132,7 +132,12 @@ struct Proj {
     if (threadIdx.x < KG) {
       const int k = threadIdx.x;
       double bias = 0.0;
-      if (!F64 && !std::is_same<T, double>::value) {
+      if (F64) {
+        // fp64 path: score = bias + sum_b w_b x_b with bias = -sum_b w_b m_b
+        // (no per-sample centring; the cancellation this leaves is ~1e-16 of
+        // sum |w m|, far below the 1e-6 plane bar)
+        for (int b = 0; b < p.bands; ++b) bias -= (double)s.w[b][k] * s.mean[b];
+      } else if (!std::is_same<T, double>::value) {
         // bias = -sum_b w_f (mean_b - hi_b): exact hi/lo split of the mean
         // (fp64 samples are centred on the full mean in fp64 instead)
         for (int b = 0; b < p.bands; ++b)
@@ -166,7 +171,7 @@ struct Proj {
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
             Acc d;
-            if constexpr (F64) d = to_f64(xs[v]) - s.mean[b];
+            if constexpr (F64) d = to_f64(xs[v]);
             else d = centred_f32<T>(xs[v], s.hi[b], s.mean[b]);
 #pragma unroll
             for (int k = 0; k < KG; ++k) acc[k][v] = fma(s.w[b][k], d, acc[k][v]);
@@ -204,7 +209,7 @@ struct Proj {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         Acc d;
-        if constexpr (F64) d = to_f64(xs[v]) - s.mean[b];
+        if constexpr (F64) d = to_f64(xs[v]);
         else d = centred_f32<T>(xs[v], s.hi[b], s.mean[b]);
 #pragma unroll
         for (int k = 0; k < KG; ++k) acc[k][v] = fma(s.w[b][k], d, acc[k][v]);
@@ -235,7 +240,7 @@ struct Proj {
     for (int b = 0; b < p.bands; ++b) {
       const T x = src[(int64_t)b * p.bs];
       Acc d;
-      if constexpr (F64) d = to_f64(x) - s.mean[b];
+      if constexpr (F64) d = to_f64(x);
       else d = centred_f32<T>(x, s.hi[b], s.mean[b]);
 #pragma unroll
       for (int k = 0; k < KG; ++k) acc[k] = fma(s.w[b][k], d, acc[k]);
@@ -574,16 +579,29 @@ stretch_kernel(const float* __restrict__ scores, const float* __restrict__ minma
   };
   auto code_of = [&](float v, const Plane& q) -> Code {
     if (q.flat) return (Code)0;
+    return code_exact(v, q);
+  };
+  // 16 codes of one plane: fp32 fast path, exact fp64 redo if any is near a tie
+  auto codes16 = [&](const float* v, const Plane& q, Code* out) {
+    if (q.flat) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) out[i] = (Code)0;
+      return;
+    }
     if constexpr (DEPTH == 8) {
-      const float x = (v - q.lof) * q.scf;
-      const float r = rintf(x);
-      if (fabsf(x - r) < 0.5f - 2e-4f) {
+      bool tie = false;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float x = (v[i] - q.lof) * q.scf;
+        tie |= fabsf(x - rintf(x)) >= 0.5f - 2e-4f;
         unsigned short u;
         asm("cvt.rni.sat.u8.f32 %0, %1;" : "=h"(u) : "f"(x));
-        return (Code)u;
+        out[i] = (Code)u;
       }
+      if (!tie) return;
     }
-    return code_exact(v, q);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) out[i] = code_exact(v[i], q);
   };
   if (vec16) {
     // plane c = blockIdx.y; 16 consecutive scores per thread per step, two
@@ -614,8 +632,7 @@ stretch_kernel(const float* __restrict__ scores, const float* __restrict__ minma
       for (int h = 0; h < 2; ++h) {
         if (h == 1 && !two) break;
         Code out[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) out[i] = code_of(v[h][i], pl);
+        codes16(v[h], pl, out);
         Code* o = dst + (q + h * step) * 16;
         st_stream_u4(o, *reinterpret_cast<const uint4*>(out));
         if constexpr (DEPTH == 16) st_stream_u4(o + 8, *reinterpret_cast<const uint4*>(out + 8));
