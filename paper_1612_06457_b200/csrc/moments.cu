@@ -7,15 +7,15 @@
 // One pass.  The n points are split into G <= 128 contiguous ranges (G is a
 // function of n only, so results do not depend on the GPU).  CTA g stages 128
 // points at a time in shared memory -- gathered straight from the cube (fused
-// pipeline) or read from a B x n design matrix -- as deviations from a local
-// pivot (the first point of each class in its range), with a constant-1 row
-// appended, and accumulates the upper triangle of [d;1][d;1]^T per class:
-// that one Gram holds the count, the shifted sums and the shifted scatter.
-// Each CTA turns its Gram into (count, mean, centred M2) per class; a second
-// kernel (one CTA per class) merges the G records in fixed order with the
-// parallel-axis rule.  Centring on a pivot keeps the one-pass form as exact as
-// the reference's two-pass form; every reduction order is fixed, so the
-// result is bit-identical run to run.
+// pipeline; the chunk's coordinates are staged first so all sample loads are
+// independent) or read from a B x n design matrix -- as deviations from the
+// class pivot (the first point of the class), with a constant-1 row appended,
+// and accumulates the upper triangle of [d;1][d;1]^T per class: one Gram holds
+// the count, the shifted sums and the shifted scatter.  A merge kernel (one
+// warp per output entry, lanes over ranges, fixed shuffle tree) sums the G
+// partials and finalizes mean = pivot + s/n, M2 = S - s s^T/n.  Centring on a
+// pivot keeps the one-pass form as accurate as the reference's two-pass form;
+// every reduction order is fixed, so results are bit-identical run to run.
 #include "common.cuh"
 
 namespace ut {
@@ -55,11 +55,17 @@ __global__ void gather_kernel(const T* __restrict__ data, int64_t bs, int64_t rs
 }
 
 // ------------------------------------------------------------------ sources
+// A source yields sample (b, j) of point j.  The cube source first stages the
+// chunk's (x, y) in shared memory so every sample load is independent.
 struct MatrixSrc {
   const double* values;
   int64_t ld;
   __device__ __forceinline__ bool valid(int64_t) const { return true; }
-  __device__ __forceinline__ double at(int b, int64_t j) const { return values[b * ld + j]; }
+  __device__ __forceinline__ void stage_xy(int64_t, int, int2*) const {}
+  __device__ __forceinline__ double at(int b, int64_t j, const int2*, int) const {
+    return values[b * ld + j];
+  }
+  __device__ __forceinline__ double at_global(int b, int64_t j) const { return values[b * ld + j]; }
 };
 
 template <typename T>
@@ -71,7 +77,18 @@ struct CubeSrc {
     const int64_t x = xy[2 * j], y = xy[2 * j + 1] - row0;
     return x >= 0 && x < cols && y >= 0 && y < rows;
   }
-  __device__ __forceinline__ double at(int b, int64_t j) const {
+  // local (x, y - row0) of points [q0, q0 + count) -> sxy[p]
+  __device__ __forceinline__ void stage_xy(int64_t q0, int count, int2* sxy) const {
+    for (int p = threadIdx.x; p < count; p += blockDim.x) {
+      const int2 v = reinterpret_cast<const int2*>(xy)[q0 + p];
+      sxy[p] = make_int2(v.x, (int)(v.y - row0));
+    }
+  }
+  __device__ __forceinline__ double at(int b, int64_t, const int2* sxy, int p) const {
+    const int2 v = sxy[p];
+    return to_f64(data[b * bs + (int64_t)v.y * rs + v.x]);
+  }
+  __device__ __forceinline__ double at_global(int b, int64_t j) const {
     const int64_t x = xy[2 * j], y = xy[2 * j + 1] - row0;
     return to_f64(data[b * bs + y * rs + x]);
   }
@@ -84,22 +101,37 @@ struct Layout {
   int64_t span;             // points per range (multiple of kChunk)
 };
 
-// per-CTA records: [c][f][g] with f in [0, 1 + B + B*B): n, mean, M2 (row-major)
 __host__ __device__ inline int rec_len(int b) { return 1 + b + b * b; }
 
 struct Smem {
   double tile[kRows * kTileLd];
   double acc[kMaxClasses * kMaxEnt];
   double pivot[kMaxClasses * kMaxBands];
+  int2 sxy[kChunk];
   int lbl[kChunk];
-  int piv_idx[kMaxClasses];
   unsigned char pi[kMaxEnt], pj[kMaxEnt];
 };
 
+// pivot[c] = first point of class c (global index), or -1
+__global__ void __launch_bounds__(1024)
+pivot_kernel(const int32_t* __restrict__ cls, int64_t n, int c0, int classes, int32_t* pivots) {
+  __shared__ int first[kMaxClasses];
+  if (threadIdx.x < classes) first[threadIdx.x] = 0x7fffffff;
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const int c = cls[j] - c0;
+    if (c >= 0 && c < classes) atomicMin(&first[c], (int)j);
+  }
+  __syncthreads();
+  if (threadIdx.x < classes)
+    pivots[threadIdx.x] = first[threadIdx.x] == 0x7fffffff ? -1 : first[threadIdx.x];
+}
+
+// Per-range Gram of [x - pivot_c ; 1] per class -> part[c][e][g] (raw sums).
 template <typename Src>
 __global__ void __launch_bounds__(kThreads)
-moments_kernel(Src src, const int32_t* __restrict__ cls, Layout L, double* __restrict__ part,
-               unsigned long long* first_bad) {
+moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restrict__ pivots,
+               Layout L, double* __restrict__ part, unsigned long long* first_bad) {
   extern __shared__ __align__(16) unsigned char raw[];
   Smem& s = *reinterpret_cast<Smem*>(raw);
   const int tid = threadIdx.x;
@@ -116,26 +148,19 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, Layout L, double* __res
     }
   }
   for (int e = tid; e < C * E; e += blockDim.x) s.acc[e] = 0.0;
-  if (tid < C) s.piv_idx[tid] = 0x7fffffff;
-  __syncthreads();
-  // local pivots: first point of each class in [j0, j1)
-  for (int64_t j = j0 + tid; j < j1; j += blockDim.x) {
-    const int c = cls[j] - L.c0;
-    if (c >= 0 && c < C && src.valid(j)) atomicMin(&s.piv_idx[c], (int)(j - j0));
-  }
-  __syncthreads();
   for (int e = tid; e < C * B; e += blockDim.x) {
     const int c = e / B, b = e - c * B;
-    const int pj = s.piv_idx[c];
-    s.pivot[e] = (pj != 0x7fffffff) ? src.at(b, j0 + pj) : 0.0;
+    const int pj = pivots[c];
+    s.pivot[e] = (pj >= 0 && src.valid(pj)) ? src.at_global(b, pj) : 0.0;
   }
   __syncthreads();
   for (int64_t q0 = j0; q0 < j1; q0 += kChunk) {
-    // stage deviations from the class pivot; row B is the constant 1
+    const int count = (int)((j1 - q0) < kChunk ? (j1 - q0) : kChunk);
+    src.stage_xy(q0, count, s.sxy);
     for (int p = tid; p < kChunk; p += blockDim.x) {
-      const int64_t j = q0 + p;
       int c = -1;
-      if (j < j1) {
+      if (p < count) {
+        const int64_t j = q0 + p;
         c = cls[j] - L.c0;
         if (c < 0 || c >= C) c = -1;
         if (!src.valid(j)) {
@@ -147,10 +172,12 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, Layout L, double* __res
       s.tile[B * kTileLd + p] = (c >= 0) ? 1.0 : 0.0;
     }
     __syncthreads();
-    for (int e = tid; e < B * kChunk; e += blockDim.x) {
-      const int b = e / kChunk, p = e - b * kChunk;
+    // deviations from the class pivot: thread -> (point p, bands b, b + 2, ...)
+    {
+      const int p = tid % kChunk;
       const int c = s.lbl[p];
-      s.tile[b * kTileLd + p] = (c >= 0) ? src.at(b, q0 + p) - s.pivot[c * B + b] : 0.0;
+      for (int b = tid / kChunk; b < B; b += kThreads / kChunk)
+        s.tile[b * kTileLd + p] = (c >= 0) ? src.at(b, q0 + p, s.sxy, p) - s.pivot[c * B + b] : 0.0;
     }
     __syncthreads();
     // Gram entries, one class run at a time (points are usually class-sorted)
@@ -159,7 +186,7 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, Layout L, double* __res
       const double* rj = s.tile + s.pj[e] * kTileLd;
       int cur = -1;
       double a = 0.0;
-      for (int p = 0; p < kChunk; ++p) {
+      for (int p = 0; p < count; ++p) {
         const int c = s.lbl[p];
         if (c < 0) continue;
         if (c != cur) {
@@ -173,94 +200,46 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, Layout L, double* __res
     }
     __syncthreads();
   }
-  // (count, mean, M2) of this range per class, written as [c][f][g]
-  const int len = rec_len(B);
   const int G = L.G;
-  for (int e = tid; e < C * len; e += blockDim.x) {
-    const int c = e / len, f = e - c * len;
-    const double* A = s.acc + c * E;
-    const int one = B;  // row of ones
-    auto ent = [&](int i, int j) {  // i <= j
-      return A[i * R - i * (i - 1) / 2 + (j - i)];
-    };
-    const double n = ent(one, one);
-    double v = 0.0;
-    if (n > 0.0) {
-      if (f == 0) {
-        v = n;
-      } else if (f <= B) {
-        const int b = f - 1;
-        v = s.pivot[c * B + b] + ent(b, one) / n;
-      } else {
-        const int q = f - 1 - B, i = q / B, j = q - i * B;
-        const int lo = i < j ? i : j, hi = i < j ? j : i;
-        v = ent(lo, hi) - ent(i, one) * ent(j, one) / n;
-      }
-    }
-    part[((size_t)c * len + f) * G + blockIdx.x] = v;
-  }
+  for (int e = tid; e < C * E; e += blockDim.x) part[(size_t)e * G + blockIdx.x] = s.acc[e];
 }
 
-// One CTA per class: merge the G range records in fixed order.
-__global__ void __launch_bounds__(1024)
-merge_kernel(const double* __restrict__ part, Layout L, double* __restrict__ moments) {
-  __shared__ double mean[kMaxBands];
-  __shared__ double cnt;
-  const int c = blockIdx.x;
+// One warp per output entry (c, f): sums the G range partials (fixed shuffle
+// tree) and finalizes count / mean = pivot + s/n / M2 = S - s s^T / n.
+template <typename Src>
+__global__ void __launch_bounds__(256)
+merge_kernel(Src src, const double* __restrict__ part, const int32_t* __restrict__ pivots,
+             Layout L, double* __restrict__ moments) {
   const int B = L.bands, G = L.G;
-  const int len = rec_len(B);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const double* P = part + (size_t)c * len * G;
-  const double* Pn = P;  // f = 0 row: counts per range
-  // counts and means (warp per field, lanes over ranges, fixed shuffle tree)
-  for (int f = warp; f <= B; f += nw) {
-    double acc = 0.0;
-    for (int g = lane; g < G; g += 32) {
-      const double n = Pn[g];
-      acc += (f == 0) ? n : (n > 0.0 ? n * P[(size_t)f * G + g] : 0.0);
-    }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      if (f == 0) cnt = acc;
-      else mean[f - 1] = acc;
-    }
-  }
-  __syncthreads();
-  const double n = cnt;
-  if (threadIdx.x < B) mean[threadIdx.x] = n > 0.0 ? mean[threadIdx.x] / n : 0.0;
-  __syncthreads();
-  double* out = moments + (size_t)(L.c0 + c) * len;
-  if (threadIdx.x == 0) out[0] = n;
-  if (threadIdx.x < B) out[1 + threadIdx.x] = mean[threadIdx.x];
-  if (G == 1) {
-    for (int q = threadIdx.x; q < B * B; q += blockDim.x) out[1 + B + q] = P[(size_t)(1 + B + q)];
-    return;
-  }
-  // M2 = sum_g [M2_g + n_g (m_g - m)(m_g - m)^T], two entries per warp step
-  for (int q0 = warp * 2; q0 < B * B; q0 += nw * 2) {
-    double acc[2] = {0.0, 0.0};
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int q = q0 + u;
-      if (q >= B * B) break;
-      const int i = q / B, j = q - i * B;
-      for (int g = lane; g < G; g += 32) {
-        const double ng = Pn[g];
-        if (ng > 0.0) {
-          const double di = P[(size_t)(1 + i) * G + g] - mean[i];
-          const double dj = P[(size_t)(1 + j) * G + g] - mean[j];
-          acc[u] += P[(size_t)(1 + B + q) * G + g] + ng * (di * dj);
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-      for (int o = 16; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
-    if (lane == 0) {
-      out[1 + B + q0] = acc[0];
-      if (q0 + 1 < B * B) out[1 + B + q0 + 1] = acc[1];
+  const int R = B + 1, E = ent_count(B), len = rec_len(B);
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= (int64_t)L.classes * len) return;
+  const int c = (int)(w / len), f = (int)(w - (int64_t)c * len);
+  auto sum = [&](int i, int j) {  // Gram entry (i, j) of class c, summed over ranges
+    if (i > j) { const int t = i; i = j; j = t; }
+    const int e = i * R - i * (i - 1) / 2 + (j - i);
+    const double* p = part + ((size_t)c * E + e) * G;
+    double a = 0.0;
+    for (int g = lane; g < G; g += 32) a += p[g];
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    return a;
+  };
+  const double n = sum(B, B);
+  double v = 0.0;
+  if (n > 0.0) {
+    if (f == 0) {
+      v = n;
+    } else if (f <= B) {
+      const int b = f - 1;
+      const int pj = pivots[c];
+      v = ((pj >= 0 && src.valid(pj)) ? src.at_global(b, pj) : 0.0) + sum(b, B) / n;
+    } else {
+      const int q = f - 1 - B, i = q / B, j = q - i * B;
+      v = sum(i, j) - sum(i, B) * sum(j, B) / n;
     }
   }
+  if (lane == 0) moments[(size_t)(L.c0 + c) * len + f] = v;
 }
 
 Layout make_layout(int64_t n, int b, int c) {
@@ -281,10 +260,8 @@ Layout make_layout(int64_t n, int b, int c) {
 
 size_t ws_bytes_for(int b, int c) {
   const int per = c < kMaxClasses ? c : kMaxClasses;
-  return sizeof(double) * (size_t)per * rec_len(b) * kMaxG + 256;
+  return sizeof(double) * (size_t)per * ent_count(b) * kMaxG + 256 + sizeof(int32_t) * 64;
 }
-
-bool g_smem_set[64] = {false};
 
 template <typename Src>
 int launch_moments(const Src& src, const int32_t* cls, int64_t n, int b, int classes,
@@ -298,13 +275,17 @@ int launch_moments(const Src& src, const int32_t* cls, int64_t n, int b, int cla
     cudaFuncSetAttribute(moments_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     attr = true;
   }
-  double* part = static_cast<double*>(ws);
+  int32_t* pivots = reinterpret_cast<int32_t*>(ws);
+  double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + 256 + sizeof(int32_t) * 64);
   for (int c0 = 0; c0 < classes; c0 += kMaxClasses) {
     Layout L = make_layout(n, b, classes - c0 < kMaxClasses ? classes - c0 : kMaxClasses);
     L.c0 = c0;
-    moments_kernel<Src><<<L.G, kThreads, bytes, st>>>(src, cls, L, part, first_bad);
+    pivot_kernel<<<1, 1024, 0, st>>>(cls, n, c0, L.classes, pivots);
+    UT_CHECK_LAUNCH("pivot_kernel");
+    moments_kernel<Src><<<L.G, kThreads, bytes, st>>>(src, cls, pivots, L, part, first_bad);
     UT_CHECK_LAUNCH("moments_kernel");
-    merge_kernel<<<L.classes, 1024, 0, st>>>(part, L, moments);
+    const int64_t warps = (int64_t)L.classes * rec_len(b);
+    merge_kernel<Src><<<(int)((warps + 7) / 8), 256, 0, st>>>(src, part, pivots, L, moments);
     UT_CHECK_LAUNCH("merge_kernel");
   }
   return UT_OK;
