@@ -103,18 +103,21 @@ int ut_gather(const ut_cube* cube, const int32_t* xy, int64_t n,
  * (two-pass, like compute_scatter's per-class loop, projection.py:187-198).
  * cls[j] in [0, classes) is the class *index* of point j (index into the sorted
  * unique labels).  moments: classes records of ut_moment_len(B) doubles:
- * [count, mean(B), M2(B*B)].  ws: ut_class_moments_ws(n, B, C) bytes. */
+ * [count, mean(B), M2(B*B)].  pivots: optional device array of C point
+ * indices (the first point of each class; NULL = found on the device) used
+ * as per-class shifts.  ws: ut_class_moments_ws(n, B, C) bytes. */
 size_t ut_class_moments_ws(int64_t n, int32_t bands, int32_t classes);
 int ut_class_moments(const double* values, int64_t ld, const int32_t* cls,
-                     int64_t n, int32_t bands, int32_t classes, double* moments,
-                     void* ws, size_t ws_bytes, void* stream);
+                     int64_t n, int32_t bands, int32_t classes, const int32_t* pivots,
+                     double* moments, void* ws, size_t ws_bytes, void* stream);
 
 /* Fused gather + class moments straight from the cube (the pipeline form of
  * assemble_matrix + compute_scatter): xy as for ut_gather; points outside the
  * (shard of the) cube are skipped and reported in first_bad (-1 if none). */
 int ut_cube_class_moments(const ut_cube* cube, const int32_t* xy, const int32_t* cls,
-                          int64_t n, int32_t classes, double* moments,
-                          int64_t* first_bad, void* ws, size_t ws_bytes, void* stream);
+                          int64_t n, int32_t classes, const int32_t* pivots,
+                          double* moments, int64_t* first_bad, void* ws, size_t ws_bytes,
+                          void* stream);
 
 /* ------------------------------------------------- K3: CVA solve
  * Combines `groups` partial moment sets (rank-major [groups][classes][len],

@@ -57,8 +57,8 @@ _SIGS = {
     "ut_moment_len": (I64, [I32]),
     "ut_gather": (I32, [C.POINTER(Cube), P, I64, P, I64, P, P]),
     "ut_class_moments_ws": (SZ, [I64, I32, I32]),
-    "ut_class_moments": (I32, [P, I64, P, I64, I32, I32, P, P, SZ, P]),
-    "ut_cube_class_moments": (I32, [C.POINTER(Cube), P, P, I64, I32, P, P, P, SZ, P]),
+    "ut_class_moments": (I32, [P, I64, P, I64, I32, I32, P, P, P, SZ, P]),
+    "ut_cube_class_moments": (I32, [C.POINTER(Cube), P, P, I64, I32, P, P, P, P, SZ, P]),
     "ut_cva_solve": (I32, [P, I32, I32, I32, F64, I32, C.POINTER(CvaOut), P]),
     "ut_gen_eig_sym": (I32, [P, P, I32, F64, P, P, P, P, P]),
     "ut_region_moments_ws": (SZ, [I32]),

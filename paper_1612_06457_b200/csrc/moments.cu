@@ -118,9 +118,13 @@ pivot_kernel(const int32_t* __restrict__ cls, int64_t n, int c0, int classes, in
   __shared__ int first[kMaxClasses];
   if (threadIdx.x < classes) first[threadIdx.x] = 0x7fffffff;
   __syncthreads();
+  unsigned seen = 0u;  // each thread's first hit per class is its minimum
   for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
     const int c = cls[j] - c0;
-    if (c >= 0 && c < classes) atomicMin(&first[c], (int)j);
+    if (c >= 0 && c < classes && !((seen >> c) & 1u)) {
+      atomicMin(&first[c], (int)j);
+      seen |= 1u << c;
+    }
   }
   __syncthreads();
   if (threadIdx.x < classes)
@@ -265,8 +269,8 @@ size_t ws_bytes_for(int b, int c) {
 
 template <typename Src>
 int launch_moments(const Src& src, const int32_t* cls, int64_t n, int b, int classes,
-                   double* moments, void* ws, size_t ws_bytes, unsigned long long* first_bad,
-                   cudaStream_t st) {
+                   const int32_t* given_pivots, double* moments, void* ws, size_t ws_bytes,
+                   unsigned long long* first_bad, cudaStream_t st) {
   UT_REQUIRE(ws_bytes >= ws_bytes_for(b, classes), "class moments: workspace %zu < %zu",
              ws_bytes, ws_bytes_for(b, classes));
   const int bytes = (int)sizeof(Smem);
@@ -280,12 +284,15 @@ int launch_moments(const Src& src, const int32_t* cls, int64_t n, int b, int cla
   for (int c0 = 0; c0 < classes; c0 += kMaxClasses) {
     Layout L = make_layout(n, b, classes - c0 < kMaxClasses ? classes - c0 : kMaxClasses);
     L.c0 = c0;
-    pivot_kernel<<<1, 1024, 0, st>>>(cls, n, c0, L.classes, pivots);
-    UT_CHECK_LAUNCH("pivot_kernel");
-    moments_kernel<Src><<<L.G, kThreads, bytes, st>>>(src, cls, pivots, L, part, first_bad);
+    const int32_t* piv = given_pivots ? given_pivots + c0 : pivots;
+    if (!given_pivots) {
+      pivot_kernel<<<1, 1024, 0, st>>>(cls, n, c0, L.classes, pivots);
+      UT_CHECK_LAUNCH("pivot_kernel");
+    }
+    moments_kernel<Src><<<L.G, kThreads, bytes, st>>>(src, cls, piv, L, part, first_bad);
     UT_CHECK_LAUNCH("moments_kernel");
     const int64_t warps = (int64_t)L.classes * rec_len(b);
-    merge_kernel<Src><<<(int)((warps + 7) / 8), 256, 0, st>>>(src, part, pivots, L, moments);
+    merge_kernel<Src><<<(int)((warps + 7) / 8), 256, 0, st>>>(src, part, piv, L, moments);
     UT_CHECK_LAUNCH("merge_kernel");
   }
   return UT_OK;
@@ -307,11 +314,13 @@ int launch_gather(const ut_cube* cube, const int32_t* xy, int64_t n, double* val
 
 template <typename T>
 int launch_cube_moments(const ut_cube* cube, const int32_t* xy, const int32_t* cls, int64_t n,
-                        int classes, double* moments, unsigned long long* first_bad, void* ws,
-                        size_t ws_bytes, cudaStream_t st) {
+                        int classes, const int32_t* pivots, double* moments,
+                        unsigned long long* first_bad, void* ws, size_t ws_bytes,
+                        cudaStream_t st) {
   CubeSrc<T> src{static_cast<const T*>(cube->data), cube->band_stride, cube->row_stride,
                  cube->rows, cube->cols, cube->row0, xy};
-  return launch_moments(src, cls, n, cube->bands, classes, moments, ws, ws_bytes, first_bad, st);
+  return launch_moments(src, cls, n, cube->bands, classes, pivots, moments, ws, ws_bytes,
+                        first_bad, st);
 }
 
 }  // namespace
@@ -347,19 +356,19 @@ size_t ut_class_moments_ws(int64_t n, int32_t bands, int32_t classes) {
 }
 
 int ut_class_moments(const double* values, int64_t ld, const int32_t* cls, int64_t n,
-                     int32_t bands, int32_t classes, double* moments, void* ws, size_t ws_bytes,
-                     void* stream) {
+                     int32_t bands, int32_t classes, const int32_t* pivots, double* moments,
+                     void* ws, size_t ws_bytes, void* stream) {
   UT_REQUIRE(bands >= 1 && bands <= kMaxBands, "ut_class_moments: bands must be 1..32");
   UT_REQUIRE(classes >= 1, "ut_class_moments: classes must be >= 1");
   UT_REQUIRE(n >= 1, "ut_class_moments: no points");
   MatrixSrc src{values, ld};
-  return launch_moments(src, cls, n, bands, classes, moments, ws, ws_bytes, nullptr,
+  return launch_moments(src, cls, n, bands, classes, pivots, moments, ws, ws_bytes, nullptr,
                         as_stream(stream));
 }
 
 int ut_cube_class_moments(const ut_cube* cube, const int32_t* xy, const int32_t* cls, int64_t n,
-                          int32_t classes, double* moments, int64_t* first_bad, void* ws,
-                          size_t ws_bytes, void* stream) {
+                          int32_t classes, const int32_t* pivots, double* moments,
+                          int64_t* first_bad, void* ws, size_t ws_bytes, void* stream) {
   UT_REQUIRE(cube && cube->bands >= 1 && cube->bands <= kMaxBands,
              "ut_cube_class_moments: bands must be 1..32");
   UT_REQUIRE(classes >= 1 && n >= 1, "ut_cube_class_moments: bad classes/points");
@@ -368,11 +377,11 @@ int ut_cube_class_moments(const ut_cube* cube, const int32_t* xy, const int32_t*
   if (e != cudaSuccess) return cuda_status(e, "ut_cube_class_moments memset");
   auto* fb = reinterpret_cast<unsigned long long*>(first_bad);
   switch (cube->dtype) {
-    case UT_U8: return launch_cube_moments<uint8_t>(cube, xy, cls, n, classes, moments, fb, ws, ws_bytes, st);
-    case UT_U16: return launch_cube_moments<uint16_t>(cube, xy, cls, n, classes, moments, fb, ws, ws_bytes, st);
-    case UT_F16: return launch_cube_moments<__half>(cube, xy, cls, n, classes, moments, fb, ws, ws_bytes, st);
-    case UT_F32: return launch_cube_moments<float>(cube, xy, cls, n, classes, moments, fb, ws, ws_bytes, st);
-    case UT_F64: return launch_cube_moments<double>(cube, xy, cls, n, classes, moments, fb, ws, ws_bytes, st);
+    case UT_U8: return launch_cube_moments<uint8_t>(cube, xy, cls, n, classes, pivots, moments, fb, ws, ws_bytes, st);
+    case UT_U16: return launch_cube_moments<uint16_t>(cube, xy, cls, n, classes, pivots, moments, fb, ws, ws_bytes, st);
+    case UT_F16: return launch_cube_moments<__half>(cube, xy, cls, n, classes, pivots, moments, fb, ws, ws_bytes, st);
+    case UT_F32: return launch_cube_moments<float>(cube, xy, cls, n, classes, pivots, moments, fb, ws, ws_bytes, st);
+    case UT_F64: return launch_cube_moments<double>(cube, xy, cls, n, classes, pivots, moments, fb, ws, ws_bytes, st);
   }
   set_error("ut_cube_class_moments: unknown dtype %d", cube->dtype);
   return UT_EDATA;

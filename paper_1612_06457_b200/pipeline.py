@@ -86,6 +86,15 @@ class CvaPipeline(_Sharded):
                 np.zeros((1, 2), np.int32)
             self.xy = dev.to_device(xy, self.device)
             self.cls = dev.to_device(cls[own] if self.n else np.zeros(1, np.int32), self.device)
+            # first local point of each class: the per-class shift of K1
+            piv = np.full(len(self.class_ids), -1, dtype=np.int32)
+            if self.n:
+                local = cls[own]
+                for c in range(len(self.class_ids)):
+                    hit = np.flatnonzero(local == c)
+                    if len(hit):
+                        piv[c] = hit[0]
+            self.pivots = dev.to_device(piv, self.device)
             self.fit = CvaDevice(b, len(self.class_ids), self.device, groups=self.world)
             self.cube = stack.cube()
             self.first_bad = torch.full((1,), -1, dtype=torch.int64, device=self.device)
@@ -101,7 +110,8 @@ class CvaPipeline(_Sharded):
 
     # -- the hot path -------------------------------------------------------
     def fit_only(self):
-        self.fit.moments_from_cube(self.cube, self.xy, self.cls, self.n, self.first_bad)
+        self.fit.moments_from_cube(self.cube, self.xy, self.cls, self.n, self.first_bad,
+                                   self.pivots)
         self.gather_moments(self.fit)
         self.fit.solve(self.ridge, self.k)
 
@@ -141,8 +151,8 @@ class CvaPipeline(_Sharded):
                                eigenvalues=np.ascontiguousarray(h["evals"][:self.k]))
 
     def launches(self) -> int:
-        """Our kernels per run(): moments + merge, solve, K4 groups, stretch."""
-        return (2 if self.n else 0) + 1 + (self.k + 7) // 8 + 1
+        """Our kernels per run(): moments + merge, solve (fast + full), K4 groups, stretch."""
+        return (2 if self.n else 0) + 2 + (self.k + 7) // 8 + 1
 
 
 class PcaPipeline(_Sharded):

@@ -191,11 +191,11 @@ class CvaDevice:
         need = L.ut_class_moments_ws(n, self.b, self.c)
         ws = dev.workspace("class_moments", need, values.device)
         _lib.check(L.ut_class_moments(values.data_ptr(), ld, cls_d.data_ptr(), n, self.b, self.c,
-                                      self.moments.data_ptr(), ws.data_ptr(), ws.numel(),
+                                      None, self.moments.data_ptr(), ws.data_ptr(), ws.numel(),
                                       dev.stream_handle()), "ut_class_moments")
 
     def moments_from_cube(self, cube, xy_d: torch.Tensor, cls_d: torch.Tensor, n: int,
-                          first_bad: torch.Tensor):
+                          first_bad: torch.Tensor, pivots: torch.Tensor | None = None):
         """Fused K1: gather the n training pixels from the cube + class moments."""
         L = _lib.lib()
         if n == 0:
@@ -204,7 +204,8 @@ class CvaDevice:
         ws = dev.workspace("class_moments", L.ut_class_moments_ws(n, self.b, self.c),
                            xy_d.device)
         _lib.check(L.ut_cube_class_moments(C.byref(cube), xy_d.data_ptr(), cls_d.data_ptr(), n,
-                                           self.c, self.moments.data_ptr(), first_bad.data_ptr(),
+                                           self.c, None if pivots is None else pivots.data_ptr(),
+                                           self.moments.data_ptr(), first_bad.data_ptr(),
                                            ws.data_ptr(), ws.numel(), dev.stream_handle()),
                    "ut_cube_class_moments")
 
