@@ -390,200 +390,96 @@ gen_eig_kernel(const double* __restrict__ A, const double* __restrict__ M, int n
   if (threadIdx.x == 0) *info = code;
 }
 
-// Low-rank CVA solve (see the header comment).  Returns false (state of s.a /
-// s.m undefined) if it cannot be used; the caller then runs the full path.
-__device__ bool cva_low_rank(Smem& s, int n, int C, double ridge, int want, ut_cva_out& out) {
-  const int tid = threadIdx.x;
-  const int i = tid / N, j = tid % N;
+// Low-rank CVA solve without triangular solves.  With W' the ridged within
+// scatter and S_b = H H^T, the nonzero eigenpairs of W'^-1 S_b come from the
+// C x C symmetric matrix T = H^T X, X = W'^-1 H:  T w = lambda w  ->
+// v = X w / sqrt(lambda), which is W'-orthonormal (v^T W' v = w^T T w / lambda).
+// X is formed by Gauss-Jordan elimination of [W' | H] -- W' is SPD, so no
+// pivoting is needed (growth factor <= 1) -- with all (row, column) updates of
+// a step in parallel: 2 barriers per step instead of the long serial chains of
+// Cholesky + two triangular solves.  Requires want <= C_live - 1 and clearly
+// nonzero wanted eigenvalues; returns false otherwise (caller: full path).
+// Expects W (unridged, symmetrized) in s.m and H in s.h.
+__device__ bool cva_low_rank_gj(Smem& s, int n, int C, double ridge, int want,
+                                ut_cva_out& out) {
+  const int tid = threadIdx.x, nt = blockDim.x;
   ridge_into_m(s, n, ridge);
-  if (tid < 32) {
-    const bool ok = chol_warp(s.m, n);
-    if (tid == 0) s.flag = ok ? 1 : 0;
+  double* f = s.x;  // elimination factors, column k
+  for (int k = 0; k < n; ++k) {
+    const double piv = s.m[k * LD + k];
+    if (!(piv > 0.0)) return false;  // uniform: W' not positive definite
+    if (tid < n) f[tid] = s.m[tid * LD + k];
+    __syncthreads();
+    const double inv = 1.0 / piv;
+    // row k / pivot (columns > k of W', all of H)
+    for (int e = tid; e < (n - 1 - k) + C; e += nt) {
+      if (e < n - 1 - k) s.m[k * LD + k + 1 + e] *= inv;
+      else s.h[k * LD + (e - (n - 1 - k))] *= inv;
+    }
+    __syncthreads();
+    // eliminate column k from every other row
+    const int wcols = (n - 1 - k) + C;
+    for (int e = tid; e < n * wcols; e += nt) {
+      const int i = e / wcols, q = e - i * wcols;
+      if (i == k) continue;
+      const double fi = f[i];
+      if (q < n - 1 - k) {
+        const int j = k + 1 + q;
+        s.m[i * LD + j] -= fi * s.m[k * LD + j];
+      } else {
+        const int c = q - (n - 1 - k);
+        s.h[i * LD + c] -= fi * s.h[k * LD + c];
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  if (!s.flag) return false;
-  if (tid < 32) fsolve_warp(s.m, s.h, n, C);  // G = L^-1 H
-  __syncthreads();
-  // T = G^T G (C x C), symmetrized, in s.a
-  if (i < C && j < C) {
+  // now s.h = X = W'^-1 H.  T = H^T X (H from the outputs), symmetrized
+  for (int e = tid; e < C * C; e += nt) {
+    const int c1 = e / C, c2 = e - c1 * C;
     double acc = 0.0;
-    for (int p = 0; p < n; ++p) acc += s.h[p * LD + i] * s.h[p * LD + j];
-    s.x[i * LD + j] = acc;
+    const double cnt = out.counts[c1];
+    if (cnt > 0.0) {
+      const double sq = sqrt(cnt);
+      for (int p = 0; p < n; ++p)
+        acc += sq * (out.class_means[c1 * n + p] - out.grand_mean[p]) * s.h[p * LD + c2];
+    }
+    s.v[c1 * LD + c2] = acc;  // scratch
   }
   __syncthreads();
-  if (i < C && j < C) s.a[i * LD + j] = 0.5 * (s.x[i * LD + j] + s.x[j * LD + i]);
+  for (int e = tid; e < C * C; e += nt) {
+    const int c1 = e / C, c2 = e - c1 * C;
+    s.a[c1 * LD + c2] = 0.5 * (s.v[c1 * LD + c2] + s.v[c2 * LD + c1]);
+  }
   __syncthreads();
   if (tid < 32) {
     const int code = jacobi_team<32>(s, s.a, s.v, C);
     if (tid == 0) s.flag = code;
   }
   __syncthreads();
-  const int jinfo = s.flag;
+  if (s.flag != 0) return false;
   sort_desc(s, s.a, C);
   const double lmax = s.a[s.order[0] * LD + s.order[0]];
   const double lw = s.a[s.order[want - 1] * LD + s.order[want - 1]];
-  if (jinfo != 0 || !(lmax > 0.0) || !(lw > 1e-12 * lmax)) return false;
-  // u_r = G w_r / sqrt(lambda_r), stored in column order[r] of s.x
-  if (i < n && j < want) {
-    const int src = s.order[j];
-    const double lam = s.a[src * LD + src];
+  if (!(lmax > 0.0) || !(lw > 1e-12 * lmax)) return false;
+  // v_r = X w_r / sqrt(lambda_r) into column order[r] of s.m (free now)
+  for (int e = tid; e < n * want; e += nt) {
+    const int i = e / want, r = e - i * want;
+    const int src = s.order[r];
     double acc = 0.0;
     for (int c = 0; c < C; ++c) acc += s.h[i * LD + c] * s.v[c * LD + src];
-    s.x[i * LD + src] = acc / sqrt(lam);
+    s.m[i * LD + src] = acc / sqrt(s.a[src * LD + src]);
   }
-  __syncthreads();
-  if (tid < 32) bsolve_warp(s.m, s.x, n, want, s.order);  // V = L^-T U
   __syncthreads();
   if (tid < n) out.evals[tid] = 0.0;  // the null space: exact zeros
   __syncthreads();
-  emit(s, s.a, s.x, n, C, want, out.evals, out.evecs);
+  emit(s, s.a, s.m, n, C, want, out.evals, out.evecs);
   return true;
 }
 
-constexpr int kMaxCw = 8;  // classes handled by the register-resident warp path
-
-// Register-resident low-rank CVA solve run by warp 0 alone (lane = matrix row).
-// The problem is padded to 32 x 32 with an identity block (exact: Cholesky,
-// G = L^-1 H and V = L^-T U are block-diagonal), so every loop is static.
-// W (unridged) in s.m, H in s.h.  Returns false if the path cannot be used.
-__device__ bool cva_low_rank_warp(Smem& s, int n, int C, double ridge, int want,
-                                  ut_cva_out& out) {
-  const unsigned F = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  double tr = 0.0;
-  for (int k = 0; k < n; ++k) tr += s.m[k * LD + k];
-  const double shift = ridge * (tr > 0.0 ? tr / n : 1.0);  // eigen.py:63-72
-  double a[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const bool diag = (j == lane);
-    a[j] = (lane < n && j < n) ? s.m[lane * LD + j] + (diag ? shift : 0.0) : (diag ? 1.0 : 0.0);
-  }
-  // Cholesky, right-looking; a[k] of lane i ends as L[i][k]
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const double akk = __shfl_sync(F, a[k], k);
-    if (!(akk > 0.0)) return false;  // uniform across the warp
-    const double lkk = sqrt(akk);
-    const double lik = (lane > k) ? a[k] / lkk : (lane == k ? lkk : 0.0);
-    a[k] = lik;
-#pragma unroll
-    for (int j = k + 1; j < 32; ++j) {
-      const double ljk = __shfl_sync(F, lik, j);
-      if (lane >= j) a[j] -= lik * ljk;
-    }
-  }
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 32; ++j) s.m[lane * LD + j] = a[j];  // L, row-major, for L^-T
-  // G = L^-1 H (lane i holds row i of H / G)
-  double g[kMaxCw];
-#pragma unroll
-  for (int c = 0; c < kMaxCw; ++c) g[c] = (lane < n && c < C) ? s.h[lane * LD + c] : 0.0;
-#pragma unroll
-  for (int p = 0; p < 32; ++p) {
-    const double inv = 1.0 / __shfl_sync(F, a[p], p);
-    const double lip = a[p];
-#pragma unroll
-    for (int c = 0; c < kMaxCw; ++c) {
-      const double xp = __shfl_sync(F, g[c], p) * inv;
-      if (lane == p) g[c] = xp;
-      else if (lane > p) g[c] -= lip * xp;
-    }
-  }
-  // T = G^T G (C x C) -> s.a; fixed xor-tree reductions
-#pragma unroll
-  for (int c1 = 0; c1 < kMaxCw; ++c1) {
-#pragma unroll
-    for (int c2 = c1; c2 < kMaxCw; ++c2) {
-      if (c2 >= C) continue;
-      double t = g[c1] * g[c2];
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(F, t, o);
-      if (lane == 0) {
-        s.a[c1 * LD + c2] = t;
-        s.a[c2 * LD + c1] = t;
-      }
-    }
-  }
-  __syncwarp();
-  if (jacobi_team<32>(s, s.a, s.v, C) != 0) return false;
-  __syncwarp();
-  if (lane < C) {
-    const double me = s.a[lane * LD + lane];
-    int rank = 0;
-    for (int o = 0; o < C; ++o) {
-      const double other = s.a[o * LD + o];
-      rank += (other > me) || (other == me && o < lane);
-    }
-    s.order[rank] = lane;
-  }
-  __syncwarp();
-  const double lmax = s.a[s.order[0] * LD + s.order[0]];
-  const double lw = s.a[s.order[want - 1] * LD + s.order[want - 1]];
-  if (!(lmax > 0.0) || !(lw > 1e-12 * lmax)) return false;
-  // u_r = G w_r / sqrt(lambda_r)
-  double u[kMaxCw];
-#pragma unroll
-  for (int r = 0; r < kMaxCw; ++r) {
-    u[r] = 0.0;
-    if (r < want) {
-      const int src = s.order[r];
-      double acc = 0.0;
-      for (int c = 0; c < C; ++c) acc += g[c] * s.v[c * LD + src];
-      u[r] = acc / sqrt(s.a[src * LD + src]);
-    }
-  }
-  __syncwarp();
-  // V = L^-T U, backward (L[p][i] from shared memory)
-#pragma unroll
-  for (int p = 31; p >= 0; --p) {
-    const double inv = 1.0 / __shfl_sync(F, a[p], p);
-    const double lpi = s.m[p * LD + lane];
-#pragma unroll
-    for (int r = 0; r < kMaxCw; ++r) {
-      const double xp = __shfl_sync(F, u[r], p) * inv;
-      if (lane == p) u[r] = xp;
-      else if (lane < p) u[r] -= lpi * xp;
-    }
-  }
-  // sign: the first largest-|entry| of each vector made positive (eigen.py:40-52)
-#pragma unroll
-  for (int r = 0; r < kMaxCw; ++r) {
-    if (r >= want) continue;
-    double best = lane < n ? fabs(u[r]) : -1.0;
-    int who = lane;
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(F, best, o);
-      const int ow = __shfl_xor_sync(F, who, o);
-      if (ob > best || (ob == best && ow < who)) { best = ob; who = ow; }
-    }
-    const double lead = __shfl_sync(F, u[r], who);
-    if (lead < 0.0) u[r] = -u[r];
-  }
-  // outputs: C eigenvalues of G^T G (descending), then exact zeros
-  if (lane < n) out.evals[lane] = lane < C ? s.a[s.order[lane] * LD + s.order[lane]] : 0.0;
-  if (lane < n) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (j >= n) break;
-      double v = 0.0;
-#pragma unroll
-      for (int r = 0; r < kMaxCw; ++r)
-        if (r == j && r < want) v = u[r];
-      out.evecs[lane * n + j] = v;
-    }
-  }
-  return true;
-}
-
-// CVA step 1 (256 threads): combine the per-group class moments, publish the
-// scatter pair, then -- when at most C-1 <= 7 leading pairs are wanted -- warp 0
-// runs the register-resident low-rank solve.  *out.info = -1 hands the problem
-// to cva_full_kernel.
 // moments: [groups][classes][1 + B + B*B] = count, mean, M2 (centred)
-__global__ void __launch_bounds__(256, 1)
-cva_fast_kernel(const double* __restrict__ mom, int groups, int n, int classes, double ridge,
-                int want, ut_cva_out out) {
+__global__ void __launch_bounds__(kThreads, 1)
+cva_solve_kernel(const double* __restrict__ mom, int groups, int n, int classes, double ridge,
+                 int want, ut_cva_out out) {
   __shared__ Smem s;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int len = 1 + n + n * n;
@@ -633,8 +529,8 @@ cva_fast_kernel(const double* __restrict__ mom, int groups, int n, int classes, 
       const double gi = mc[i] - out.grand_mean[i], gj = mc[j] - out.grand_mean[j];
       b += out.counts[c] * (gi * gj);
     }
-    s.m[i * LD + j] = w;
-    s.a[i * LD + j] = b;
+    s.x[i * LD + j] = w;
+    s.v[i * LD + j] = b;
   }
   // H = [sqrt(n_c) (m_c - m)] for the low-rank path
   for (int e = tid; e < n * classes && classes <= kMaxC; e += nt) {
@@ -647,58 +543,26 @@ cva_fast_kernel(const double* __restrict__ mom, int groups, int n, int classes, 
   // symmetrize both (projection.py:199-200) and publish the scatter pair
   for (int e = tid; e < n * n; e += nt) {
     const int i = e / n, j = e - i * n;
-    out.within[e] = 0.5 * (s.m[i * LD + j] + s.m[j * LD + i]);
-    out.between[e] = 0.5 * (s.a[i * LD + j] + s.a[j * LD + i]);
-  }
-  __syncthreads();
-  for (int e = tid; e < n * n; e += nt) {
-    const int i = e / n, j = e - i * n;
-    s.m[i * LD + j] = out.within[e];
-  }
-  __syncthreads();
-  int live = 0;
-  for (int c = 0; c < classes; ++c) live += out.counts[c] > 0.0;
-  bool done = false;
-  if (classes <= kMaxCw && classes <= n && want >= 1 && want <= live - 1) {
-    if (tid < 32) {
-      const bool ok = cva_low_rank_warp(s, n, classes, ridge, want, out);
-      if (tid == 0) s.flag = ok ? 1 : 0;
-    }
-    __syncthreads();
-    done = s.flag != 0;
-  }
-  if (tid == 0) *out.info = done ? 0 : -1;
-}
-
-// CVA step 2 (1024 threads): only if step 1 left *out.info == -1 -- the smem
-// low-rank path for up to 32 classes, else the full B x B generalized solve.
-__global__ void __launch_bounds__(kThreads, 1)
-cva_full_kernel(int n, int classes, double ridge, int want, ut_cva_out out) {
-  if (*out.info != -1) return;
-  __shared__ Smem s;
-  const int tid = threadIdx.x;
-  const int i = tid / N, j = tid % N;
-  if (i < n && j < n) {
-    s.m[i * LD + j] = out.within[i * n + j];
-    s.a[i * LD + j] = out.between[i * n + j];
-  }
-  if (classes <= kMaxC && i < n && j < classes) {
-    const double cnt = out.counts[j];
-    s.h[i * LD + j] =
-        cnt > 0.0 ? sqrt(cnt) * (out.class_means[j * n + i] - out.grand_mean[i]) : 0.0;
+    const double w = 0.5 * (s.x[i * LD + j] + s.x[j * LD + i]);
+    const double b = 0.5 * (s.v[i * LD + j] + s.v[j * LD + i]);
+    s.m[i * LD + j] = w;
+    s.a[i * LD + j] = b;
+    out.within[e] = w;
+    out.between[e] = b;
   }
   __syncthreads();
   int live = 0;
   for (int c = 0; c < classes; ++c) live += out.counts[c] > 0.0;
   if (classes <= kMaxC && classes <= n && want >= 1 && want <= live - 1) {
-    if (cva_low_rank(s, n, classes, ridge, want, out)) {
+    if (cva_low_rank_gj(s, n, classes, ridge, want, out)) {
       if (tid == 0) *out.info = 0;
       return;
     }
     __syncthreads();  // fall back: restore W and S_b
-    if (i < n && j < n) {
-      s.m[i * LD + j] = out.within[i * n + j];
-      s.a[i * LD + j] = out.between[i * n + j];
+    for (int e = tid; e < n * n; e += nt) {
+      const int i = e / n, j = e - i * n;
+      s.m[i * LD + j] = out.within[e];
+      s.a[i * LD + j] = out.between[e];
     }
     __syncthreads();
   }
@@ -784,11 +648,9 @@ int ut_cva_solve(const double* moments, int32_t groups, int32_t bands, int32_t c
   UT_REQUIRE(bands >= 1 && bands <= kMaxBands, "ut_cva_solve: bands must be 1..32");
   UT_REQUIRE(groups >= 1 && classes >= 1, "ut_cva_solve: bad groups/classes");
   UT_REQUIRE(out, "ut_cva_solve: null output");
-  cudaStream_t st = as_stream(stream);
-  cva_fast_kernel<<<1, 256, 0, st>>>(moments, groups, bands, classes, ridge, want, *out);
-  UT_CHECK_LAUNCH("cva_fast_kernel");
-  cva_full_kernel<<<1, kThreads, 0, st>>>(bands, classes, ridge, want, *out);
-  UT_CHECK_LAUNCH("cva_full_kernel");
+  cva_solve_kernel<<<1, kThreads, 0, as_stream(stream)>>>(moments, groups, bands, classes, ridge,
+                                                          want, *out);
+  UT_CHECK_LAUNCH("cva_solve_kernel");
   return UT_OK;
 }
 

@@ -60,6 +60,10 @@ __global__ void gather_kernel(const T* __restrict__ data, int64_t bs, int64_t rs
 struct MatrixSrc {
   const double* values;
   int64_t ld;
+  using Coord = int64_t;
+  __device__ __forceinline__ Coord coord(int64_t j) const { return j; }
+  __device__ __forceinline__ bool valid_at(Coord) const { return true; }
+  __device__ __forceinline__ double sample(int b, Coord j) const { return values[b * ld + j]; }
   __device__ __forceinline__ bool valid(int64_t) const { return true; }
   __device__ __forceinline__ void stage_xy(int64_t, int, int2*) const {}
   __device__ __forceinline__ double at(int b, int64_t j, const int2*, int) const {
@@ -73,6 +77,17 @@ struct CubeSrc {
   const T* data;
   int64_t bs, rs, rows, cols, row0;
   const int32_t* xy;
+  using Coord = int2;  // (x, local y)
+  __device__ __forceinline__ Coord coord(int64_t j) const {
+    const int2 v = reinterpret_cast<const int2*>(xy)[j];
+    return make_int2(v.x, (int)(v.y - row0));
+  }
+  __device__ __forceinline__ bool valid_at(Coord c) const {
+    return c.x >= 0 && c.x < cols && c.y >= 0 && c.y < rows;
+  }
+  __device__ __forceinline__ double sample(int b, Coord c) const {
+    return to_f64(data[b * bs + (int64_t)c.y * rs + c.x]);
+  }
   __device__ __forceinline__ bool valid(int64_t j) const {
     const int64_t x = xy[2 * j], y = xy[2 * j + 1] - row0;
     return x >= 0 && x < cols && y >= 0 && y < rows;
@@ -107,8 +122,8 @@ struct Smem {
   double tile[kRows * kTileLd];
   double acc[kMaxClasses * kMaxEnt];
   double pivot[kMaxClasses * kMaxBands];
-  int2 sxy[kChunk];
   int lbl[kChunk];
+  unsigned mask;
   unsigned char pi[kMaxEnt], pj[kMaxEnt];
 };
 
@@ -158,49 +173,82 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restri
     s.pivot[e] = (pj >= 0 && src.valid(pj)) ? src.at_global(b, pj) : 0.0;
   }
   __syncthreads();
+  // Staging: thread -> point p = tid % 128, bands tid/128, +2, +4, ...  The
+  // next chunk's samples are loaded into registers while the current chunk's
+  // Gram is accumulated (the gather is random-access, latency-bound).
+  constexpr int kPer = kMaxBands / (kThreads / kChunk);  // 16 bands per thread
+  const int sp = tid % kChunk, sb = tid / kChunk;
+  double nv[kPer];
+  int nl = -1;
+  auto prefetch = [&](int64_t q0) {
+    const int64_t j = q0 + sp;
+    nl = -1;
+    if (j < j1) {
+      const typename Src::Coord cc = src.coord(j);
+      int c = cls[j] - L.c0;
+      if (c < 0 || c >= C) c = -1;
+      if (!src.valid_at(cc)) {
+        if (first_bad && sb == 0) atomicMin(first_bad, (unsigned long long)j);
+        c = -1;
+      }
+      nl = c;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int b = sb + u * (kThreads / kChunk);
+        nv[u] = (c >= 0 && b < B) ? src.sample(b, cc) : 0.0;
+      }
+    }
+  };
+  if (j0 < j1) prefetch(j0);
   for (int64_t q0 = j0; q0 < j1; q0 += kChunk) {
     const int count = (int)((j1 - q0) < kChunk ? (j1 - q0) : kChunk);
-    src.stage_xy(q0, count, s.sxy);
-    for (int p = tid; p < kChunk; p += blockDim.x) {
-      int c = -1;
-      if (p < count) {
-        const int64_t j = q0 + p;
-        c = cls[j] - L.c0;
-        if (c < 0 || c >= C) c = -1;
-        if (!src.valid(j)) {
-          if (first_bad) atomicMin(first_bad, (unsigned long long)j);
-          c = -1;
-        }
-      }
-      s.lbl[p] = c;
-      s.tile[B * kTileLd + p] = (c >= 0) ? 1.0 : 0.0;
+    if (tid == 0) s.mask = 0u;
+    __syncthreads();
+    // deviations from the class pivot; row B is the constant 1 (0 for padding)
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int b = sb + u * (kThreads / kChunk);
+      if (b < B) s.tile[b * kTileLd + sp] = (nl >= 0) ? nv[u] - s.pivot[nl * B + b] : 0.0;
+    }
+    if (sb == 0) {
+      s.lbl[sp] = nl;
+      s.tile[B * kTileLd + sp] = (nl >= 0) ? 1.0 : 0.0;
+      if (nl >= 0) atomicOr(&s.mask, 1u << nl);
     }
     __syncthreads();
-    // deviations from the class pivot: thread -> (point p, bands b, b + 2, ...)
-    {
-      const int p = tid % kChunk;
-      const int c = s.lbl[p];
-      for (int b = tid / kChunk; b < B; b += kThreads / kChunk)
-        s.tile[b * kTileLd + p] = (c >= 0) ? src.at(b, q0 + p, s.sxy, p) - s.pivot[c * B + b] : 0.0;
-    }
-    __syncthreads();
-    // Gram entries, one class run at a time (points are usually class-sorted)
-    for (int e = tid; e < E; e += blockDim.x) {
-      const double* ri = s.tile + s.pi[e] * kTileLd;
-      const double* rj = s.tile + s.pj[e] * kTileLd;
-      int cur = -1;
-      double a = 0.0;
-      for (int p = 0; p < count; ++p) {
-        const int c = s.lbl[p];
-        if (c < 0) continue;
-        if (c != cur) {
-          if (cur >= 0) s.acc[cur * E + e] = a;
-          cur = c;
-          a = s.acc[c * E + e];
-        }
-        a = fma(ri[p], rj[p], a);
+    if (q0 + kChunk < j1) prefetch(q0 + kChunk);
+    const unsigned mask = s.mask;
+    if (mask != 0u && (mask & (mask - 1u)) == 0u) {
+      // one class in this chunk (class-sorted points): branch-free loop;
+      // padding / foreign points are zero rows and add nothing
+      const int c = __ffs(mask) - 1;
+      for (int e = tid; e < E; e += blockDim.x) {
+        const double* ri = s.tile + s.pi[e] * kTileLd;
+        const double* rj = s.tile + s.pj[e] * kTileLd;
+        double a = s.acc[c * E + e];
+#pragma unroll 8
+        for (int p = 0; p < kChunk; ++p) a = fma(ri[p], rj[p], a);
+        s.acc[c * E + e] = a;
       }
-      if (cur >= 0) s.acc[cur * E + e] = a;
+    } else if (mask != 0u) {
+      // mixed chunk: one class run at a time
+      for (int e = tid; e < E; e += blockDim.x) {
+        const double* ri = s.tile + s.pi[e] * kTileLd;
+        const double* rj = s.tile + s.pj[e] * kTileLd;
+        int cur = -1;
+        double a = 0.0;
+        for (int p = 0; p < count; ++p) {
+          const int c = s.lbl[p];
+          if (c < 0) continue;
+          if (c != cur) {
+            if (cur >= 0) s.acc[cur * E + e] = a;
+            cur = c;
+            a = s.acc[c * E + e];
+          }
+          a = fma(ri[p], rj[p], a);
+        }
+        if (cur >= 0) s.acc[cur * E + e] = a;
+      }
     }
     __syncthreads();
   }

@@ -151,8 +151,8 @@ class CvaPipeline(_Sharded):
                                eigenvalues=np.ascontiguousarray(h["evals"][:self.k]))
 
     def launches(self) -> int:
-        """Our kernels per run(): moments + merge, solve (fast + full), K4 groups, stretch."""
-        return (2 if self.n else 0) + 2 + (self.k + 7) // 8 + 1
+        """Our kernels per run(): moments + merge, solve, K4 groups, stretch."""
+        return (2 if self.n else 0) + 1 + (self.k + 7) // 8 + 1
 
 
 class PcaPipeline(_Sharded):
