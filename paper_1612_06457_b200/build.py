@@ -56,6 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
               "-I", str(INCLUDE), "--expt-relaxed-constexpr"]
     if verbose:
         common += ["-Xptxas", "-v"]
+    common += os.environ.get("UT_NVCC_FLAGS", "").split()  # e.g. -DUT_PHASES (dev)
 
     def compile_one(src: Path) -> Path:
         obj = OBJ_DIR / (src.stem + ".o")

@@ -31,6 +31,22 @@ constexpr int kThreads = N * N;  // 1024 (combine steps use all of them)
 constexpr int kTeam = 128;       // Jacobi team
 constexpr int kMaxC = 32;        // classes handled by the low-rank path
 
+#ifdef UT_PHASES  // dev builds: per-phase %globaltimer stamps of thread 0
+__device__ unsigned long long g_eig_phase[32];
+#define EPH(i)                                                     \
+  do {                                                             \
+    if (threadIdx.x == 0) {                                        \
+      unsigned long long _t;                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));       \
+      g_eig_phase[(i)] = _t;                                       \
+    }                                                              \
+  } while (0)
+#else
+#define EPH(i) \
+  do {         \
+  } while (0)
+#endif
+
 struct Smem {
   double a[N * LD];   // working matrix (A, then C, then Jacobi iterate)
   double m[N * LD];   // M (then L)
@@ -403,6 +419,7 @@ gen_eig_kernel(const double* __restrict__ A, const double* __restrict__ M, int n
 __device__ bool cva_low_rank_gj(Smem& s, int n, int C, double ridge, int want,
                                 ut_cva_out& out) {
   const int tid = threadIdx.x, nt = blockDim.x;
+  EPH(5);
   ridge_into_m(s, n, ridge);
   double* f = s.x;  // elimination factors, column k
   for (int k = 0; k < n; ++k) {
@@ -433,6 +450,7 @@ __device__ bool cva_low_rank_gj(Smem& s, int n, int C, double ridge, int want,
     }
     __syncthreads();
   }
+  EPH(6);
   // now s.h = X = W'^-1 H.  T = H^T X (H from the outputs), symmetrized
   for (int e = tid; e < C * C; e += nt) {
     const int c1 = e / C, c2 = e - c1 * C;
@@ -451,11 +469,13 @@ __device__ bool cva_low_rank_gj(Smem& s, int n, int C, double ridge, int want,
     s.a[c1 * LD + c2] = 0.5 * (s.v[c1 * LD + c2] + s.v[c2 * LD + c1]);
   }
   __syncthreads();
+  EPH(7);
   if (tid < 32) {
     const int code = jacobi_team<32>(s, s.a, s.v, C);
     if (tid == 0) s.flag = code;
   }
   __syncthreads();
+  EPH(8);
   if (s.flag != 0) return false;
   sort_desc(s, s.a, C);
   const double lmax = s.a[s.order[0] * LD + s.order[0]];
@@ -470,9 +490,11 @@ __device__ bool cva_low_rank_gj(Smem& s, int n, int C, double ridge, int want,
     s.m[i * LD + src] = acc / sqrt(s.a[src * LD + src]);
   }
   __syncthreads();
+  EPH(9);
   if (tid < n) out.evals[tid] = 0.0;  // the null space: exact zeros
   __syncthreads();
   emit(s, s.a, s.m, n, C, want, out.evals, out.evecs);
+  EPH(10);
   return true;
 }
 
@@ -483,6 +505,7 @@ cva_solve_kernel(const double* __restrict__ mom, int groups, int n, int classes,
   __shared__ Smem s;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int len = 1 + n + n * n;
+  EPH(0);
   // per class: pooled count / mean (parallel-axis rule across groups)
   for (int e = tid; e < classes * (1 + n); e += nt) {
     const int c = e / (1 + n), f = e - c * (1 + n);
@@ -502,6 +525,7 @@ cva_solve_kernel(const double* __restrict__ mom, int groups, int n, int classes,
     }
   }
   __syncthreads();
+  EPH(1);
   // grand mean = sum_c n_c m_c / N
   if (tid < n) {
     double tot = 0.0, acc = 0.0;
@@ -512,6 +536,7 @@ cva_solve_kernel(const double* __restrict__ mom, int groups, int n, int classes,
     out.grand_mean[tid] = acc / tot;
   }
   __syncthreads();
+  EPH(2);
   // within = sum_c [sum_g M2_gc + n_gc (m_gc - m_c)(m_gc - m_c)^T]
   // between = sum_c n_c (m_c - m)(m_c - m)^T     (projection.py:196-198)
   for (int e = tid; e < n * n; e += nt) {
@@ -540,6 +565,7 @@ cva_solve_kernel(const double* __restrict__ mom, int groups, int n, int classes,
         cnt > 0.0 ? sqrt(cnt) * (out.class_means[c * n + i] - out.grand_mean[i]) : 0.0;
   }
   __syncthreads();
+  EPH(3);
   // symmetrize both (projection.py:199-200) and publish the scatter pair
   for (int e = tid; e < n * n; e += nt) {
     const int i = e / n, j = e - i * n;
@@ -551,6 +577,7 @@ cva_solve_kernel(const double* __restrict__ mom, int groups, int n, int classes,
     out.between[e] = b;
   }
   __syncthreads();
+  EPH(4);
   int live = 0;
   for (int c = 0; c < classes; ++c) live += out.counts[c] > 0.0;
   if (classes <= kMaxC && classes <= n && want >= 1 && want <= live - 1) {
@@ -632,6 +659,13 @@ pca_solve_kernel(const double* __restrict__ mom, int groups, int n, ut_pca_out o
 using namespace ut;
 
 extern "C" {
+
+#ifdef UT_PHASES
+int ut_debug_eig_phases(unsigned long long* host) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(host, g_eig_phase, sizeof(g_eig_phase)) == cudaSuccess ? 0 : 3;
+}
+#endif
 
 int ut_gen_eig_sym(const double* A, const double* M, int32_t bands, double ridge, double* evals,
                    double* evecs, double* aux, int32_t* info, void* stream) {

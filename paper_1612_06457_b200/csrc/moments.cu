@@ -61,9 +61,12 @@ struct MatrixSrc {
   const double* values;
   int64_t ld;
   using Coord = int64_t;
+  using Raw = double;
   __device__ __forceinline__ Coord coord(int64_t j) const { return j; }
   __device__ __forceinline__ bool valid_at(Coord) const { return true; }
   __device__ __forceinline__ double sample(int b, Coord j) const { return values[b * ld + j]; }
+  __device__ __forceinline__ Raw raw(int b, Coord j) const { return values[b * ld + j]; }
+  __device__ __forceinline__ static double widen(Raw v) { return v; }
   __device__ __forceinline__ bool valid(int64_t) const { return true; }
   __device__ __forceinline__ void stage_xy(int64_t, int, int2*) const {}
   __device__ __forceinline__ double at(int b, int64_t j, const int2*, int) const {
@@ -78,6 +81,11 @@ struct CubeSrc {
   int64_t bs, rs, rows, cols, row0;
   const int32_t* xy;
   using Coord = int2;  // (x, local y)
+  using Raw = T;
+  __device__ __forceinline__ Raw raw(int b, Coord c) const {
+    return data[b * bs + (int64_t)c.y * rs + c.x];
+  }
+  __device__ __forceinline__ static double widen(Raw v) { return to_f64(v); }
   __device__ __forceinline__ Coord coord(int64_t j) const {
     const int2 v = reinterpret_cast<const int2*>(xy)[j];
     return make_int2(v.x, (int)(v.y - row0));
@@ -174,32 +182,44 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restri
   }
   __syncthreads();
   // Staging: thread -> point p = tid % 128, bands tid/128, +2, +4, ...  The
-  // next chunk's samples are loaded into registers while the current chunk's
-  // Gram is accumulated (the gather is random-access, latency-bound).
+  // gather is random-access and latency-bound, so it is software-pipelined:
+  // coordinates / labels are loaded two chunks ahead and raw samples one chunk
+  // ahead (kept unconverted in registers), while the current chunk's Gram runs.
   constexpr int kPer = kMaxBands / (kThreads / kChunk);  // 16 bands per thread
   const int sp = tid % kChunk, sb = tid / kChunk;
-  double nv[kPer];
-  int nl = -1;
-  auto prefetch = [&](int64_t q0) {
+  typename Src::Raw nv[kPer];
+  int nl = -1;                     // label of the chunk in nv
+  typename Src::Coord ncc{};       // coordinates two chunks ahead
+  int nnl = -1;
+  auto load_coord = [&](int64_t q0) {
     const int64_t j = q0 + sp;
-    nl = -1;
+    nnl = -1;
     if (j < j1) {
-      const typename Src::Coord cc = src.coord(j);
+      ncc = src.coord(j);
       int c = cls[j] - L.c0;
       if (c < 0 || c >= C) c = -1;
-      if (!src.valid_at(cc)) {
-        if (first_bad && sb == 0) atomicMin(first_bad, (unsigned long long)j);
-        c = -1;
-      }
-      nl = c;
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int b = sb + u * (kThreads / kChunk);
-        nv[u] = (c >= 0 && b < B) ? src.sample(b, cc) : 0.0;
-      }
+      nnl = c;
     }
   };
-  if (j0 < j1) prefetch(j0);
+  auto load_samples = [&](int64_t q0) {  // uses the coordinates loaded for q0
+    const int64_t j = q0 + sp;
+    int c = nnl;
+    if (j < j1 && c >= 0 && !src.valid_at(ncc)) {
+      if (first_bad && sb == 0) atomicMin(first_bad, (unsigned long long)j);
+      c = -1;
+    }
+    nl = (j < j1) ? c : -1;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int b = sb + u * (kThreads / kChunk);
+      nv[u] = (nl >= 0 && b < B) ? src.raw(b, ncc) : typename Src::Raw(0);
+    }
+  };
+  if (j0 < j1) {
+    load_coord(j0);
+    load_samples(j0);
+    if (j0 + kChunk < j1) load_coord(j0 + kChunk);
+  }
   for (int64_t q0 = j0; q0 < j1; q0 += kChunk) {
     const int count = (int)((j1 - q0) < kChunk ? (j1 - q0) : kChunk);
     if (tid == 0) s.mask = 0u;
@@ -208,7 +228,8 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restri
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const int b = sb + u * (kThreads / kChunk);
-      if (b < B) s.tile[b * kTileLd + sp] = (nl >= 0) ? nv[u] - s.pivot[nl * B + b] : 0.0;
+      if (b < B)
+        s.tile[b * kTileLd + sp] = (nl >= 0) ? Src::widen(nv[u]) - s.pivot[nl * B + b] : 0.0;
     }
     if (sb == 0) {
       s.lbl[sp] = nl;
@@ -216,7 +237,8 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restri
       if (nl >= 0) atomicOr(&s.mask, 1u << nl);
     }
     __syncthreads();
-    if (q0 + kChunk < j1) prefetch(q0 + kChunk);
+    if (q0 + kChunk < j1) load_samples(q0 + kChunk);
+    if (q0 + 2 * kChunk < j1) load_coord(q0 + 2 * kChunk);
     const unsigned mask = s.mask;
     if (mask != 0u && (mask & (mask - 1u)) == 0u) {
       // one class in this chunk (class-sorted points): branch-free loop;
