@@ -103,7 +103,10 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
     const int i = e / n, j = e - i * n;
     v[i * LD + j] = (i == j) ? 1.0 : 0.0;
   }
-  // absolute floor: off-diagonals below 1e-22 * ||A||_F count as zero
+  // absolute floor: off-diagonals below eps/2 * ||A||_F count as zero.  They
+  // move eigenvalues by at most that much (<< the 1e-9 * lambda_max bar) and
+  // rounding noise at this level in rank-deficient matrices (the CVA null
+  // space) would otherwise keep the sweeps going.
   double fro = 0.0;
   for (int e = t; e < n * n; e += NT) {
     const int i = e / n, j = e - i * n;
@@ -115,7 +118,7 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
   double f = 0.0;
   for (int w = 0; w < NT / 32; ++w) f += s.red[w];
   team_sync<NT>();
-  const double floor_abs = 1e-22 * sqrt(f);
+  const double floor_abs = 0.5 * DBL_EPSILON * sqrt(f);
   if (n < 2) return 0;
   const int m = n + (n & 1);
   const int half = m / 2;
@@ -421,35 +424,35 @@ __device__ bool cva_low_rank_gj(Smem& s, int n, int C, double ridge, int want,
   const int tid = threadIdx.x, nt = blockDim.x;
   EPH(5);
   ridge_into_m(s, n, ridge);
-  double* f = s.x;  // elimination factors, column k
-  for (int k = 0; k < n; ++k) {
-    const double piv = s.m[k * LD + k];
-    if (!(piv > 0.0)) return false;  // uniform: W' not positive definite
-    if (tid < n) f[tid] = s.m[tid * LD + k];
-    __syncthreads();
-    const double inv = 1.0 / piv;
-    // row k / pivot (columns > k of W', all of H)
-    for (int e = tid; e < (n - 1 - k) + C; e += nt) {
-      if (e < n - 1 - k) s.m[k * LD + k + 1 + e] *= inv;
-      else s.h[k * LD + (e - (n - 1 - k))] *= inv;
-    }
-    __syncthreads();
-    // eliminate column k from every other row
-    const int wcols = (n - 1 - k) + C;
-    for (int e = tid; e < n * wcols; e += nt) {
-      const int i = e / wcols, q = e - i * wcols;
-      if (i == k) continue;
-      const double fi = f[i];
-      if (q < n - 1 - k) {
-        const int j = k + 1 + q;
-        s.m[i * LD + j] -= fi * s.m[k * LD + j];
-      } else {
-        const int c = q - (n - 1 - k);
-        s.h[i * LD + c] -= fi * s.h[k * LD + c];
+  // one warp, lane = row; rows of [W' | H] in shared memory
+  if (tid < 32) {
+    const int lane = tid;
+    int ok = 1;
+    for (int k = 0; k < n; ++k) {
+      const double piv = s.m[k * LD + k];
+      if (!(piv > 0.0)) {  // uniform: W' not positive definite
+        ok = 0;
+        break;
       }
+      const double inv = 1.0 / piv;
+      const double fi = lane < n ? s.m[lane * LD + k] : 0.0;
+      __syncwarp();
+      if (lane == k) {
+        for (int j = k + 1; j < n; ++j) s.m[k * LD + j] *= inv;
+        for (int c = 0; c < C; ++c) s.h[k * LD + c] *= inv;
+      }
+      __syncwarp();
+      if (lane < n && lane != k) {
+#pragma unroll 4
+        for (int j = k + 1; j < n; ++j) s.m[lane * LD + j] -= fi * s.m[k * LD + j];
+        for (int c = 0; c < C; ++c) s.h[lane * LD + c] -= fi * s.h[k * LD + c];
+      }
+      __syncwarp();
     }
-    __syncthreads();
+    if (tid == 0) s.flag = ok;
   }
+  __syncthreads();
+  if (!s.flag) return false;
   EPH(6);
   // now s.h = X = W'^-1 H.  T = H^T X (H from the outputs), symmetrized
   for (int e = tid; e < C * C; e += nt) {

@@ -42,7 +42,7 @@ def main():
         pipe.check()
         f = pipe.fit
         t_mom = timed(lambda: f.moments_from_cube(pipe.cube, pipe.xy, pipe.cls, pipe.n,
-                                                  pipe.first_bad))
+                                                  pipe.first_bad, pipe.pivots))
         t_fast = timed(lambda: f.solve(1e-8, cfg.k))
         t_full = timed(lambda: f.solve(1e-8, 0))
         t_proj = timed(pipe.project_kernel)
