@@ -137,25 +137,32 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
           q = (r - k + (m - 1)) % (m - 1);
         }
         if (p > q) { const int tmp = p; p = q; q = tmp; }
-        double c = 1.0, sn = 0.0, npp = 0.0, nqq = 0.0;
+        double c = 1.0, sn = 0.0;
         int act = 0;
         if (q < n) {
           const double apq = a[p * LD + q];
           const double app = a[p * LD + p], aqq = a[q * LD + q];
           const double thr = fmax(0.5 * DBL_EPSILON * sqrt(fabs(app) * fabs(aqq)), floor_abs);
           if (fabs(apq) > thr) {
-            const double theta = (aqq - app) / (2.0 * apq);
-            double tt;
-            if (fabs(theta) > 1e150) {
-              tt = 0.5 / theta;
+            // Rutishauser's angle evaluated in fp32 (short latency chain); the
+            // rotation itself is made orthogonal to fp64 accuracy below and the
+            // 2x2 block is rotated exactly, so the angle's precision only
+            // affects how far a_pq drops per step, not the result.
+            const float theta = (float)((aqq - app) / (2.0 * apq));
+            float tf;
+            if (fabsf(theta) > 1e18f) {
+              tf = 0.5f / theta;
             } else {
-              tt = 1.0 / (fabs(theta) + sqrt(1.0 + theta * theta));
-              if (theta < 0.0) tt = -tt;
+              tf = 1.0f / (fabsf(theta) + sqrtf(fmaf(theta, theta, 1.0f)));
+              if (theta < 0.0f) tf = -tf;
             }
-            c = 1.0 / sqrt(1.0 + tt * tt);
-            sn = tt * c;
-            npp = app - tt * apq;
-            nqq = aqq + tt * apq;
+            const double tt = (double)tf;
+            const double x = fma(tt, tt, 1.0);
+            double r = (double)rsqrtf((float)x);      // 1/sqrt(1 + t^2): fp32 guess,
+            r = r * fma(-0.5 * x, r * r, 1.5);        // two Newton steps in fp64
+            r = r * fma(-0.5 * x, r * r, 1.5);
+            c = r;
+            sn = tt * r;
             act = 1;
           }
         }
@@ -163,8 +170,6 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
         s.qq[k] = q;
         s.cs[k] = c;
         s.sn[k] = sn;
-        s.npp[k] = npp;
-        s.nqq[k] = nqq;
         rotated |= act;
       }
       team_sync<NT>();
@@ -181,24 +186,16 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
         }
       }
       team_sync<NT>();
-      // phase C: columns p, q <- A J (exact 2x2 block written), V <- V J
+      // phase C: columns p, q <- A J, V <- V J
       for (int e = t; e < half * n; e += NT) {
         const int k = e / n, row = e - k * n;
         const int p = s.pp[k];
         if (p >= 0) {
           const int q = s.qq[k];
           const double c = s.cs[k], sn = s.sn[k];
-          if (row == p) {
-            a[p * LD + p] = s.npp[k];
-            a[p * LD + q] = 0.0;
-          } else if (row == q) {
-            a[q * LD + p] = 0.0;
-            a[q * LD + q] = s.nqq[k];
-          } else {
-            const double ap = a[row * LD + p], aq = a[row * LD + q];
-            a[row * LD + p] = c * ap - sn * aq;
-            a[row * LD + q] = sn * ap + c * aq;
-          }
+          const double ap = a[row * LD + p], aq = a[row * LD + q];
+          a[row * LD + p] = c * ap - sn * aq;
+          a[row * LD + q] = sn * ap + c * aq;
           const double vp = v[row * LD + p], vq = v[row * LD + q];
           v[row * LD + p] = c * vp - sn * vq;
           v[row * LD + q] = sn * vp + c * vq;
@@ -424,7 +421,9 @@ __device__ bool cva_low_rank_gj(Smem& s, int n, int C, double ridge, int want,
   const int tid = threadIdx.x, nt = blockDim.x;
   EPH(5);
   ridge_into_m(s, n, ridge);
-  // one warp, lane = row; rows of [W' | H] in shared memory
+  // one warp, lane = row; rows of [W' | H] in shared memory.  Row k is not
+  // normalized (each lane scales its own factor by 1/pivot), so a step needs
+  // one warp barrier; the pivots are divided out at the end.
   if (tid < 32) {
     const int lane = tid;
     int ok = 1;
@@ -434,20 +433,18 @@ __device__ bool cva_low_rank_gj(Smem& s, int n, int C, double ridge, int want,
         ok = 0;
         break;
       }
-      const double inv = 1.0 / piv;
-      const double fi = lane < n ? s.m[lane * LD + k] : 0.0;
-      __syncwarp();
-      if (lane == k) {
-        for (int j = k + 1; j < n; ++j) s.m[k * LD + j] *= inv;
-        for (int c = 0; c < C; ++c) s.h[k * LD + c] *= inv;
-      }
+      const double g = lane < n ? s.m[lane * LD + k] * __drcp_rn(piv) : 0.0;
       __syncwarp();
       if (lane < n && lane != k) {
 #pragma unroll 4
-        for (int j = k + 1; j < n; ++j) s.m[lane * LD + j] -= fi * s.m[k * LD + j];
-        for (int c = 0; c < C; ++c) s.h[lane * LD + c] -= fi * s.h[k * LD + c];
+        for (int j = k + 1; j < n; ++j) s.m[lane * LD + j] -= g * s.m[k * LD + j];
+        for (int c = 0; c < C; ++c) s.h[lane * LD + c] -= g * s.h[k * LD + c];
       }
       __syncwarp();
+    }
+    if (ok && lane < n) {
+      const double d = s.m[lane * LD + lane];
+      for (int c = 0; c < C; ++c) s.h[lane * LD + c] /= d;
     }
     if (tid == 0) s.flag = ok;
   }

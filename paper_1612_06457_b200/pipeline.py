@@ -79,6 +79,11 @@ class CvaPipeline(_Sharded):
         self.k = _top_k(k, stack.band_count)
         self.ridge, self.precision, self.depth = float(ridge), precision, depth
         own = route_points(ys, stack.row0, stack.height) if self.world > 1 else np.arange(len(xs))
+        # K1 visits the points grouped by class and, within a class, in raster
+        # order: class runs keep its Gram loop branch-free and row order keeps
+        # the random gather TLB-/sector-friendly (the sums' order is fixed by
+        # this permutation, so results stay deterministic)
+        own = own[np.lexsort((xs[own], ys[own], cls[own]))]
         self.n = len(own)
         b = stack.band_count
         with torch.cuda.device(self.device):
