@@ -103,10 +103,10 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
     const int i = e / n, j = e - i * n;
     v[i * LD + j] = (i == j) ? 1.0 : 0.0;
   }
-  // absolute floor: off-diagonals below eps/2 * ||A||_F count as zero.  They
-  // move eigenvalues by at most that much (<< the 1e-9 * lambda_max bar) and
-  // rounding noise at this level in rank-deficient matrices (the CVA null
-  // space) would otherwise keep the sweeps going.
+  // absolute floor: off-diagonals below 1e-14 * ||A||_F count as zero.  They
+  // move eigenvalues by at most that much (<< the 1e-9 * lambda_max bar), and
+  // rounding noise of a few eps * ||A|| in rank-deficient matrices (the CVA
+  // null space) would otherwise keep the sweeps going.
   double fro = 0.0;
   for (int e = t; e < n * n; e += NT) {
     const int i = e / n, j = e - i * n;
@@ -118,11 +118,11 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
   double f = 0.0;
   for (int w = 0; w < NT / 32; ++w) f += s.red[w];
   team_sync<NT>();
-  const double floor_abs = 0.5 * DBL_EPSILON * sqrt(f);
+  const double floor_abs = 1e-14 * sqrt(f);
   if (n < 2) return 0;
   const int m = n + (n & 1);
   const int half = m / 2;
-  for (int sweep = 0; sweep < 60; ++sweep) {
+  for (int sweep = 0; sweep < 40; ++sweep) {
     int rotated = 0;
     for (int r = 0; r < m - 1; ++r) {
       // phase A: rotation of pair k (Rutishauser's stable formulas)
@@ -421,33 +421,33 @@ __device__ bool cva_low_rank_gj(Smem& s, int n, int C, double ridge, int want,
   const int tid = threadIdx.x, nt = blockDim.x;
   EPH(5);
   ridge_into_m(s, n, ridge);
-  // one warp, lane = row; rows of [W' | H] in shared memory.  Row k is not
-  // normalized (each lane scales its own factor by 1/pivot), so a step needs
-  // one warp barrier; the pivots are divided out at the end.
-  if (tid < 32) {
-    const int lane = tid;
-    int ok = 1;
-    for (int k = 0; k < n; ++k) {
-      const double piv = s.m[k * LD + k];
-      if (!(piv > 0.0)) {  // uniform: W' not positive definite
-        ok = 0;
-        break;
-      }
-      const double g = lane < n ? s.m[lane * LD + k] * __drcp_rn(piv) : 0.0;
-      __syncwarp();
-      if (lane < n && lane != k) {
-#pragma unroll 4
-        for (int j = k + 1; j < n; ++j) s.m[lane * LD + j] -= g * s.m[k * LD + j];
-        for (int c = 0; c < C; ++c) s.h[lane * LD + c] -= g * s.h[k * LD + c];
-      }
-      __syncwarp();
+  // Whole CTA, one barrier per step: every (row i != k, column j > k) entry of
+  // [W' | H] is updated in parallel with its own factor m[i][k] / m[k][k];
+  // row k is left unnormalized and the pivots are divided out at the end.
+  const int wl = n + C;  // columns of [W' | H]
+  for (int k = 0; k < n; ++k) {
+    const double piv = s.m[k * LD + k];
+    if (!(piv > 0.0)) {  // uniform: W' not positive definite
+      if (tid == 0) s.flag = 0;
+      __syncthreads();
+      return false;
     }
-    if (ok && lane < n) {
-      const double d = s.m[lane * LD + lane];
-      for (int c = 0; c < C; ++c) s.h[lane * LD + c] /= d;
+    const double inv = __drcp_rn(piv);
+    const int w = wl - (k + 1);  // columns > k
+    for (int e = tid; e < n * w; e += nt) {
+      const int i = e / w, q = k + 1 + (e - i * w);
+      if (i == k) continue;
+      const double g = s.m[i * LD + k] * inv;
+      if (q < n) s.m[i * LD + q] -= g * s.m[k * LD + q];
+      else s.h[i * LD + (q - n)] -= g * s.h[k * LD + (q - n)];
     }
-    if (tid == 0) s.flag = ok;
+    __syncthreads();
   }
+  for (int e = tid; e < n * C; e += nt) {
+    const int i = e / C, c = e - i * C;
+    s.h[i * LD + c] /= s.m[i * LD + i];
+  }
+  if (tid == 0) s.flag = 1;
   __syncthreads();
   if (!s.flag) return false;
   EPH(6);

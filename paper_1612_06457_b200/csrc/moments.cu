@@ -4,7 +4,7 @@
 // (annotations.py:195-215) and compute_scatter's per-class reductions
 // (projection.py:187-198).
 //
-// One pass.  The n points are split into G <= 128 contiguous ranges (G is a
+// One pass.  The n points are split into G <= 1024 contiguous ranges (G is a
 // function of n only, so results do not depend on the GPU).  CTA g stages 128
 // points at a time in shared memory -- gathered straight from the cube (fused
 // pipeline; the chunk's coordinates are staged first so all sample loads are
@@ -23,8 +23,8 @@ namespace {
 
 constexpr int kChunk = 128;      // points staged per step
 constexpr int kThreads = 256;
-constexpr int kMaxG = 128;       // point ranges (CTAs)
-constexpr int kMinPerCta = 64;
+constexpr int kMaxG = 1024;      // point ranges (CTAs)
+constexpr int kMinPerCta = 128;  // one staged chunk per CTA when n <= 128 * 1024
 constexpr int kMaxClasses = 16;  // per launch; more classes -> several launches
 constexpr int kRows = kMaxBands + 1;                    // bands + ones row
 constexpr int kMaxEnt = kRows * (kRows + 1) / 2;        // 561
@@ -126,14 +126,40 @@ struct Layout {
 
 __host__ __device__ inline int rec_len(int b) { return 1 + b + b * b; }
 
+// Shared memory, sized for the launch's B and C (dynamic):
+//   tile[(B+1) x kTileLd] | acc[C x E] | pivot[C x B] | lbl[kChunk] | mask | pi, pj[E]
 struct Smem {
-  double tile[kRows * kTileLd];
-  double acc[kMaxClasses * kMaxEnt];
-  double pivot[kMaxClasses * kMaxBands];
-  int lbl[kChunk];
-  unsigned mask;
-  unsigned char pi[kMaxEnt], pj[kMaxEnt];
+  double* tile;
+  double* acc;
+  double* pivot;
+  int* lbl;
+  unsigned* mask_p;
+  unsigned char* pi;
+  unsigned char* pj;
 };
+
+__host__ __device__ inline size_t smem_bytes(int b, int c) {
+  const int E = ent_count(b);
+  size_t off = sizeof(double) * ((size_t)(b + 1) * kTileLd + (size_t)c * E + (size_t)c * b);
+  off += sizeof(int) * kChunk + 16;
+  off += 2 * (size_t)E;
+  return (off + 15) & ~(size_t)15;
+}
+
+__device__ inline Smem carve(unsigned char* raw, int b, int c) {
+  const int E = ent_count(b);
+  Smem s;
+  double* d = reinterpret_cast<double*>(raw);
+  s.tile = d;
+  s.acc = d + (size_t)(b + 1) * kTileLd;
+  s.pivot = s.acc + (size_t)c * E;
+  int* ip = reinterpret_cast<int*>(s.pivot + (size_t)c * b);
+  s.lbl = ip;
+  s.mask_p = reinterpret_cast<unsigned*>(ip + kChunk);
+  s.pi = reinterpret_cast<unsigned char*>(s.mask_p + 4);
+  s.pj = s.pi + E;
+  return s;
+}
 
 // pivot[c] = first point of class c (global index), or -1
 __global__ void __launch_bounds__(1024)
@@ -160,7 +186,7 @@ __global__ void __launch_bounds__(kThreads)
 moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restrict__ pivots,
                Layout L, double* __restrict__ part, unsigned long long* first_bad) {
   extern __shared__ __align__(16) unsigned char raw[];
-  Smem& s = *reinterpret_cast<Smem*>(raw);
+  const Smem s = carve(raw, L.bands, L.classes);
   const int tid = threadIdx.x;
   const int B = L.bands, C = L.classes;
   const int R = B + 1;
@@ -222,7 +248,7 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restri
   }
   for (int64_t q0 = j0; q0 < j1; q0 += kChunk) {
     const int count = (int)((j1 - q0) < kChunk ? (j1 - q0) : kChunk);
-    if (tid == 0) s.mask = 0u;
+    if (tid == 0) *s.mask_p = 0u;
     __syncthreads();
     // deviations from the class pivot; row B is the constant 1 (0 for padding)
 #pragma unroll
@@ -234,12 +260,12 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restri
     if (sb == 0) {
       s.lbl[sp] = nl;
       s.tile[B * kTileLd + sp] = (nl >= 0) ? 1.0 : 0.0;
-      if (nl >= 0) atomicOr(&s.mask, 1u << nl);
+      if (nl >= 0) atomicOr(s.mask_p, 1u << nl);
     }
     __syncthreads();
     if (q0 + kChunk < j1) load_samples(q0 + kChunk);
     if (q0 + 2 * kChunk < j1) load_coord(q0 + 2 * kChunk);
-    const unsigned mask = s.mask;
+    const unsigned mask = *s.mask_p;
     if (mask != 0u && (mask & (mask - 1u)) == 0u) {
       // one class in this chunk (class-sorted points): branch-free loop;
       // padding / foreign points are zero rows and add nothing
@@ -343,11 +369,13 @@ int launch_moments(const Src& src, const int32_t* cls, int64_t n, int b, int cla
                    unsigned long long* first_bad, cudaStream_t st) {
   UT_REQUIRE(ws_bytes >= ws_bytes_for(b, classes), "class moments: workspace %zu < %zu",
              ws_bytes, ws_bytes_for(b, classes));
-  const int bytes = (int)sizeof(Smem);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(moments_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    attr = true;
+  static int attr = 0;
+  const int full = (int)smem_bytes(b, classes < kMaxClasses ? classes : kMaxClasses);
+  if (attr < full) {
+    cudaError_t e = cudaFuncSetAttribute(moments_kernel<Src>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, full);
+    if (e != cudaSuccess) return cuda_status(e, "moments smem attribute");
+    attr = full;
   }
   int32_t* pivots = reinterpret_cast<int32_t*>(ws);
   double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + 256 + sizeof(int32_t) * 64);
@@ -359,7 +387,8 @@ int launch_moments(const Src& src, const int32_t* cls, int64_t n, int b, int cla
       pivot_kernel<<<1, 1024, 0, st>>>(cls, n, c0, L.classes, pivots);
       UT_CHECK_LAUNCH("pivot_kernel");
     }
-    moments_kernel<Src><<<L.G, kThreads, bytes, st>>>(src, cls, piv, L, part, first_bad);
+    moments_kernel<Src><<<L.G, kThreads, smem_bytes(b, L.classes), st>>>(src, cls, piv, L, part,
+                                                                        first_bad);
     UT_CHECK_LAUNCH("moments_kernel");
     const int64_t warps = (int64_t)L.classes * rec_len(b);
     merge_kernel<Src><<<(int)((warps + 7) / 8), 256, 0, st>>>(src, part, piv, L, moments);
