@@ -118,14 +118,14 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
   double f = 0.0;
   for (int w = 0; w < NT / 32; ++w) f += s.red[w];
   team_sync<NT>();
-  const double floor_abs = 1e-14 * sqrt(f);
+  const double floor2 = 1e-28 * f;  // (1e-14 ||A||_F)^2
   if (n < 2) return 0;
   const int m = n + (n & 1);
   const int half = m / 2;
   for (int sweep = 0; sweep < 40; ++sweep) {
     int rotated = 0;
     for (int r = 0; r < m - 1; ++r) {
-      // phase A: rotation of pair k (Rutishauser's stable formulas)
+      // phase A: rotation of pair k (Rutishauser's formulas; round-robin pairs)
       if (t < half) {
         const int k = t;
         int p, q;
@@ -133,8 +133,10 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
           p = m - 1;
           q = r;
         } else {
-          p = (r + k) % (m - 1);
-          q = (r - k + (m - 1)) % (m - 1);
+          p = r + k;
+          if (p >= m - 1) p -= m - 1;
+          q = r - k + (m - 1);
+          if (q >= m - 1) q -= m - 1;
         }
         if (p > q) { const int tmp = p; p = q; q = tmp; }
         double c = 1.0, sn = 0.0;
@@ -142,27 +144,30 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
         if (q < n) {
           const double apq = a[p * LD + q];
           const double app = a[p * LD + p], aqq = a[q * LD + q];
-          const double thr = fmax(0.5 * DBL_EPSILON * sqrt(fabs(app) * fabs(aqq)), floor_abs);
-          if (fabs(apq) > thr) {
-            // Rutishauser's angle evaluated in fp32 (short latency chain); the
-            // rotation itself is made orthogonal to fp64 accuracy below and the
-            // 2x2 block is rotated exactly, so the angle's precision only
-            // affects how far a_pq drops per step, not the result.
-            const float theta = (float)((aqq - app) / (2.0 * apq));
-            float tf;
-            if (fabsf(theta) > 1e18f) {
-              tf = 0.5f / theta;
+          // |a_pq| > max(eps/2 sqrt(|a_pp a_qq|), floor), squared (no sqrt)
+          const double apq2 = apq * apq;
+          if (apq2 > 0.25 * DBL_EPSILON * DBL_EPSILON * fabs(app * aqq) && apq2 > floor2) {
+            // The angle is evaluated in fp32 (short latency chain) on scaled
+            // operands; the rotation is then made orthogonal to fp64 accuracy
+            // and applied as a full similarity, so the angle's precision only
+            // sets how far a_pq drops per step, not the result.
+            const double big = fmax(fabs(aqq - app), 2.0 * fabs(apq));
+            const double sc = 1.0 / big;
+            const float num = (float)((aqq - app) * sc), den = (float)(2.0 * apq * sc);
+            double tt;
+            if (fabsf(den) < 1e-18f * fabsf(num)) {
+              tt = apq / (aqq - app);  // theta beyond fp32: t ~ 1 / (2 theta)
             } else {
-              tf = 1.0f / (fabsf(theta) + sqrtf(fmaf(theta, theta, 1.0f)));
-              if (theta < 0.0f) tf = -tf;
+              const float theta = num / den;
+              float tf = 1.0f / (fabsf(theta) + sqrtf(fmaf(theta, theta, 1.0f)));
+              tt = (double)(theta < 0.0f ? -tf : tf);
             }
-            const double tt = (double)tf;
             const double x = fma(tt, tt, 1.0);
-            double r = (double)rsqrtf((float)x);      // 1/sqrt(1 + t^2): fp32 guess,
-            r = r * fma(-0.5 * x, r * r, 1.5);        // two Newton steps in fp64
-            r = r * fma(-0.5 * x, r * r, 1.5);
-            c = r;
-            sn = tt * r;
+            double rr = (double)rsqrtf((float)x);  // 1/sqrt(1 + t^2): fp32 guess,
+            rr = rr * fma(-0.5 * x, rr * rr, 1.5);  // two Newton steps in fp64
+            rr = rr * fma(-0.5 * x, rr * rr, 1.5);
+            c = rr;
+            sn = tt * rr;
             act = 1;
           }
         }

@@ -27,3 +27,4 @@ for name, h, w in (("cfg1", 512, 512), ("cfg4", 1024, 1024)):
     t = np.array(list(buf), dtype=np.float64)
     t0 = t[0]
     print(cfg.name, [round((t[i] - t0) / 1000, 1) for i in range(11)], "us")
+    print("   sweeps:", [round((t[i] - t0) / 1000, 1) for i in range(11, 31) if t[i] > t0])
