@@ -253,7 +253,7 @@ def run_reference(args):
         "value": round(value, 3), "unit": "Mpixel/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "bands": cfg.bands, "classes": cfg.classes,
                    "components": cfg.k, "pixels": cfg.pixels},
         "cpu_baseline": {"value": round(value, 3), "unit": "Mpixel/s", "cores": cores,
@@ -390,7 +390,7 @@ def run_b200(args):
             else "PCA Mpixel/s (covariance+eigen+projection)",
             "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak" if world > 1 else "weak",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f64" if pipe_precision(args) == "fp64" else "f32 (fit f64)",
             "data": "synthetic (BASELINE.json generator, generated in HBM; seed %d)" % cfg.seed,
