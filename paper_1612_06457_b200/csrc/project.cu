@@ -171,7 +171,7 @@ struct Proj {
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
             Acc d;
-            if constexpr (F64) d = to_f64(xs[v]);
+            if constexpr (F64) d = widen_f64(xs[v]);
             else d = centred_f32<T>(xs[v], s.hi[b], s.mean[b]);
 #pragma unroll
             for (int k = 0; k < KG; ++k) acc[k][v] = fma(s.w[b][k], d, acc[k][v]);
@@ -209,7 +209,7 @@ struct Proj {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         Acc d;
-        if constexpr (F64) d = to_f64(xs[v]);
+        if constexpr (F64) d = widen_f64(xs[v]);
         else d = centred_f32<T>(xs[v], s.hi[b], s.mean[b]);
 #pragma unroll
         for (int k = 0; k < KG; ++k) acc[k][v] = fma(s.w[b][k], d, acc[k][v]);
@@ -240,7 +240,7 @@ struct Proj {
     for (int b = 0; b < p.bands; ++b) {
       const T x = src[(int64_t)b * p.bs];
       Acc d;
-      if constexpr (F64) d = to_f64(x);
+      if constexpr (F64) d = widen_f64(x);
       else d = centred_f32<T>(x, s.hi[b], s.mean[b]);
 #pragma unroll
       for (int k = 0; k < KG; ++k) acc[k] = fma(s.w[b][k], d, acc[k]);

@@ -492,3 +492,37 @@ def test_stretch_ties_and_boundaries_bit_exact():
         got16 = stretch_planes(scores, mm, depth=16).cpu().numpy().reshape(-1)
         want16 = oracle.linear_to_codes(plane.astype(np.float64), lo32, hi32, 16)
         assert np.array_equal(got16, want16), (lo, hi)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float16, np.uint16, np.uint8, np.float64])
+def test_fp64_projector_widening_exact(dtype):
+    """The fp64 projector widens samples without F2F/I2F (bit tricks); check it
+    against the oracle on awkward values: zeros, negatives, large magnitudes."""
+    rng = np.random.default_rng(21)
+    shape = (5, 33, 47)
+    if dtype in (np.uint16, np.uint8):
+        top = 65535 if dtype == np.uint16 else 255
+        cube = rng.integers(0, top + 1, size=shape).astype(dtype)
+        cube[:, 0, :] = 0
+        cube[:, 1, :] = top
+    else:
+        cube = (rng.normal(size=shape) * 100).astype(dtype)
+        cube[:, 0, :5] = 0
+        cube[:, 2, :3] = -0.0
+        cube[1, 3, :4] = 1e-3
+    coef = rng.normal(size=(5, 3))
+    mean = rng.normal(size=5)
+    model = ut.ProjectionModel("cva", mean, None, coef, np.ones(3))
+    depth = 16 if dtype == np.uint16 else 8
+    stack = ut.SpectralStack(ut.stack.default_bands(5), cube, depth, normalized=True) \
+        if dtype in (np.uint16, np.uint8) else None
+    if stack is None:
+        ds = ut.DeviceStack(ut.stack.default_bands(5), torch.from_numpy(cube).cuda(), 8, True)
+        planes = [p.values.double().cpu().numpy() for p in ut.project_stack(ds, model,
+                                                                              precision="fp64")]
+    else:
+        planes = [p.values for p in ut.project_stack(stack, model, precision="fp64")]
+    ref = oracle.project(cube, {"mean": mean, "std": None, "coefficients": coef})
+    for got, want in zip(planes, ref):
+        rng_ = float(want.max() - want.min())
+        assert float(np.abs(got - want).max()) <= 1e-7 * rng_
