@@ -420,6 +420,175 @@ project_tma_kernel(ProjParams p, int P, int R) {
   Pj::finish(p, s, mn, mx, chk);
 }
 
+// ------------------------------------------------------- K4 (TMA + DMMA)
+// fp64 projection on the FP64 tensor cores: scores (8 x px) = W^T (8 x 4) x
+// X (4 x px) + bias, one mma.sync.m8n8k4.f64 per 4 bands x 8 pixels.  M = the
+// (<= 8) components of this pass, K = bands, N = pixels.  The A fragments (the
+// weights) stay in registers for the whole kernel; every sample is read from
+// the shared-memory stage and widened to fp64 exactly once (B fragments).  Same
+// producer / 3-stage bulk-copy ring as project_tma_kernel; 8 consumer warps,
+// each owning 64 pixels (8 MMA column groups) of a 512-pixel tile.
+constexpr int kDmmaCons = 256;
+constexpr int kDmmaGroups = 8;                       // 8-pixel groups per warp per tile
+constexpr int kDmmaP = (kDmmaCons / 32) * kDmmaGroups * 8;  // 512 pixels per tile
+
+template <typename T> constexpr int dmma_pad() { return 32 / (int)sizeof(T); }  // 32 B
+
+template <typename T>
+size_t dmma_smem(int bands) {
+  const int ps = kDmmaP + dmma_pad<T>();
+  return (size_t)kTmaStages * bands * ps * sizeof(T) + 2 * kTmaStages * sizeof(uint64_t) + 128;
+}
+
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <typename T, int KG>
+__global__ void __launch_bounds__(kDmmaCons + 32, 1)
+project_dmma_kernel(ProjParams p) {
+  using Pj = Proj<T, 1, KG, true>;
+  __shared__ typename Pj::Smem s;
+  extern __shared__ __align__(128) unsigned char dyn[];
+  const int B = p.bands;
+  constexpr int PS = kDmmaP + dmma_pad<T>();  // padded stage row (bank spread)
+  T* stages = reinterpret_cast<T*>(dyn);
+  uint64_t* full = reinterpret_cast<uint64_t*>(dyn + (size_t)kTmaStages * B * PS * sizeof(T));
+  uint64_t* empty = full + kTmaStages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < kTmaStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kDmmaCons / 32);
+    }
+    mbar_fence_init();
+  }
+  Pj::setup(p, s);  // fp64 weights and bias in shared memory (all threads)
+  const int64_t ntiles = (p.npix + kDmmaP - 1) / kDmmaP;
+  float mn[KG], mx[KG], chk = 0.0f;
+#pragma unroll
+  for (int k = 0; k < KG; ++k) {
+    mn[k] = INFINITY;
+    mx[k] = -INFINITY;
+  }
+  if (warp == kDmmaCons / 32) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int i = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int st = i % kTmaStages;
+        const uint32_t ph = (uint32_t)(i / kTmaStages) & 1u;
+        if (i >= kTmaStages) mbar_wait(&empty[st], ph ^ 1u);
+        const int64_t p0 = t * kDmmaP;
+        const int64_t npx = (p.npix - p0) < kDmmaP ? (p.npix - p0) : kDmmaP;
+        const uint32_t bytes = (uint32_t)(npx * sizeof(T));
+        mbar_expect_tx(&full[st], bytes * (uint32_t)B);
+        T* dst = stages + (size_t)st * B * PS;
+        const T* src = static_cast<const T*>(p.data) + p0;
+        for (int b = 0; b < B; ++b)
+          bulk_g2s(dst + (size_t)b * PS, src + (int64_t)b * p.bs, bytes, &full[st], pol);
+      }
+    }
+  } else {
+    // A fragments: A[m = lane/4][k = lane%4] = w[band 4q + lane%4][comp lane/4]
+    const int am = lane >> 2, ak = lane & 3;
+    double afrag[kMaxBands / 4];
+#pragma unroll
+    for (int q = 0; q < kMaxBands / 4; ++q) {
+      const int b = 4 * q + ak;
+      afrag[q] = (am < KG && b < B) ? (double)s.w[b][am] : 0.0;
+    }
+    const double bias = am < KG ? (double)s.bias[am] : 0.0;
+    const int nq = (B + 3) / 4;
+    float lmn = INFINITY, lmx = -INFINITY;  // this lane's component am
+    int i = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int st = i % kTmaStages;
+      const uint32_t ph = (uint32_t)(i / kTmaStages) & 1u;
+      mbar_wait(&full[st], ph);
+      const int64_t p0 = t * kDmmaP;
+      const int64_t npx = (p.npix - p0) < kDmmaP ? (p.npix - p0) : kDmmaP;
+      const T* stage = stages + (size_t)st * B * PS;
+      const int wp0 = warp * (kDmmaGroups * 8);  // this warp's first pixel in the tile
+      double c0[kDmmaGroups], c1[kDmmaGroups];
+#pragma unroll
+      for (int g = 0; g < kDmmaGroups; ++g) c0[g] = c1[g] = 0.0;
+      // B fragment: B[k = lane%4][n = lane/4] = x[band 4q + lane%4][pixel n]
+      const int bk = lane & 3, bn = lane >> 2;
+#pragma unroll
+      for (int q = 0; q < kMaxBands / 4; ++q) {
+        if (q < nq) {
+          const int b = 4 * q + bk;
+          const T* row = stage + (size_t)(b < B ? b : 0) * PS + wp0 + bn;
+#pragma unroll
+          for (int g = 0; g < kDmmaGroups; ++g) {
+            const double x = b < B ? widen_f64(row[8 * g]) : 0.0;
+            dmma_884(c0[g], c1[g], afrag[q], x);
+          }
+        }
+      }
+      // C[m = lane/4][n = 2 (lane%4) + {0,1}] -> scores of component m
+      if (am < KG) {
+        const int cn = 2 * (lane & 3);
+#pragma unroll
+        for (int g = 0; g < kDmmaGroups; ++g) {
+          const int lp = wp0 + 8 * g + cn;
+          if (lp + 2 <= npx) {
+            float o[2] = {(float)(c0[g] + bias), (float)(c1[g] + bias)};
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              lmn = fminf(lmn, o[v]);
+              lmx = fmaxf(lmx, o[v]);
+              chk = nan_guard(chk, o[v]);
+            }
+            store_scores<2>(p.scores + (int64_t)(p.k0 + am) * p.npix + p0 + lp, o);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+#pragma unroll
+    for (int k = 0; k < KG; ++k)
+      if (k == am) {
+        mn[k] = lmn;
+        mx[k] = lmx;
+      }
+  }
+  Pj::finish(p, s, mn, mx, chk);
+}
+
+template <typename T, int KG>
+int launch_dmma(ProjParams& p, cudaStream_t st) {
+  auto kern = project_dmma_kernel<T, KG>;
+  const size_t smem = dmma_smem<T>(p.bands);
+  static size_t attr = 0;
+  if (attr < smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "project_dmma smem attribute");
+    attr = smem;
+  }
+  const int64_t ntiles = (p.npix + kDmmaP - 1) / kDmmaP;
+  int64_t grid = sm_count();
+  if (grid > ntiles) grid = ntiles;
+  if (grid < 1) grid = 1;
+  kern<<<(int)grid, kDmmaCons + 32, smem, st>>>(p);
+  UT_CHECK_LAUNCH("project_dmma_kernel");
+  return UT_OK;
+}
+
+bool dmma_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("UT_PROJECT_DMMA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 bool tma_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -491,6 +660,9 @@ int launch_kg(ProjParams& p, bool vector_ok, cudaStream_t st) {
     // fp64 accumulation is FMA-pipe heavy: 8 consumer warps, 2-4 pixels each;
     // fp32: 4 consumer warps with 16-byte groups.
     if constexpr (F64) {
+      // even pixel count: scores are stored as aligned float2 pairs
+      if (dmma_enabled() && dmma_smem<T>(p.bands) <= 227 * 1024 && (p.npix % 2) == 0)
+        return launch_dmma<T, KG>(p, st);
       constexpr int VT = (16 / (int)sizeof(T)) < 2 ? 1 : ((8 / (int)sizeof(T)) < 2 ? 2 : 8 / (int)sizeof(T));
       if ((p.npix % VT) == 0) return launch_tma<T, VT, KG, F64, 256>(p, st);
     } else {
