@@ -429,14 +429,15 @@ project_tma_kernel(ProjParams p, int P, int R) {
 // producer / 3-stage bulk-copy ring as project_tma_kernel; 8 consumer warps,
 // each owning 64 pixels (8 MMA column groups) of a 512-pixel tile.
 constexpr int kDmmaCons = 256;
-constexpr int kDmmaGroups = 8;                       // 8-pixel groups per warp per tile
-constexpr int kDmmaP = (kDmmaCons / 32) * kDmmaGroups * 8;  // 512 pixels per tile
-
+// 8-pixel MMA column groups per warp per tile: 64 pixels for 4/8-byte samples,
+// 128 for 1/2-byte samples (keeps each band's bulk copy >= 2 KB)
+template <typename T> constexpr int dmma_groups() { return sizeof(T) >= 4 ? 8 : 16; }
+template <typename T> constexpr int dmma_p() { return (kDmmaCons / 32) * dmma_groups<T>() * 8; }
 template <typename T> constexpr int dmma_pad() { return 32 / (int)sizeof(T); }  // 32 B
 
 template <typename T>
 size_t dmma_smem(int bands) {
-  const int ps = kDmmaP + dmma_pad<T>();
+  const int ps = dmma_p<T>() + dmma_pad<T>();
   return (size_t)kTmaStages * bands * ps * sizeof(T) + 2 * kTmaStages * sizeof(uint64_t) + 128;
 }
 
@@ -453,6 +454,8 @@ project_dmma_kernel(ProjParams p) {
   __shared__ typename Pj::Smem s;
   extern __shared__ __align__(128) unsigned char dyn[];
   const int B = p.bands;
+  constexpr int kDmmaGroups = dmma_groups<T>();
+  constexpr int kDmmaP = dmma_p<T>();
   constexpr int PS = kDmmaP + dmma_pad<T>();  // padded stage row (bank spread)
   T* stages = reinterpret_cast<T*>(dyn);
   uint64_t* full = reinterpret_cast<uint64_t*>(dyn + (size_t)kTmaStages * B * PS * sizeof(T));
@@ -571,7 +574,7 @@ int launch_dmma(ProjParams& p, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_status(e, "project_dmma smem attribute");
     attr = smem;
   }
-  const int64_t ntiles = (p.npix + kDmmaP - 1) / kDmmaP;
+  const int64_t ntiles = (p.npix + dmma_p<T>() - 1) / dmma_p<T>();
   int64_t grid = sm_count();
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
@@ -661,7 +664,10 @@ int launch_kg(ProjParams& p, bool vector_ok, cudaStream_t st) {
     // fp32: 4 consumer warps with 16-byte groups.
     if constexpr (F64) {
       // even pixel count: scores are stored as aligned float2 pairs
-      if (dmma_enabled() && dmma_smem<T>(p.bands) <= 227 * 1024 && (p.npix % 2) == 0)
+      // DMMA pads the components to M = 8: worth it from 4 components up, and for
+      // 4/8-byte samples (2-byte samples make the tile compute-bound)
+      if (dmma_enabled() && sizeof(T) >= 4 && KG >= 4 && dmma_smem<T>(p.bands) <= 227 * 1024 &&
+          (p.npix % 2) == 0)
         return launch_dmma<T, KG>(p, st);
       constexpr int VT = (16 / (int)sizeof(T)) < 2 ? 1 : ((8 / (int)sizeof(T)) < 2 ? 2 : 8 / (int)sizeof(T));
       if ((p.npix % VT) == 0) return launch_tma<T, VT, KG, F64, 256>(p, st);

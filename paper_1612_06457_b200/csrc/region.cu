@@ -16,6 +16,8 @@
 // pixels.  fp64-FMA-bound for B = 32 (561 DFMA per pixel), HBM-bound for
 // B <= 16.  Partials are summed by a separate kernel, one warp per entry,
 // lanes over CTAs, in a fixed shuffle tree: deterministic.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ut {
@@ -39,7 +41,7 @@ struct RegionWs {
 size_t region_ws_layout(RegionWs* ws, void* base) {
   const size_t off_shift = 256;
   const size_t off_part = off_shift + sizeof(double) * kMaxBands;
-  const size_t total = off_part + sizeof(double) * (size_t)kMaxG * kEnt;
+  const size_t total = off_part + sizeof(double) * (size_t)kMaxG * kEnt;  // >= 1056 x 592 (DMMA path)
   if (ws && base) {
     char* p = static_cast<char*>(base);
     ws->shift = reinterpret_cast<double*>(p + off_shift);
@@ -224,6 +226,247 @@ region_merge_kernel(Region r, RegionWs ws, double* __restrict__ moments) {
   if (lane == 0) moments[e] = v;
 }
 
+// ---------------------------------------------------- K2 on FP64 tensor cores
+// Whole-width regions (contiguous pixel range): a producer warp streams
+// [B][512]-pixel tiles into a 3-stage shared-memory ring with bulk async
+// copies; 8 consumer warps each take 4-pixel quads and, per 8-band group g,
+// load one fragment element per lane -- x[band 8g + lane/4][pixel lane%4] --
+// widen it, subtract the shift, and issue mma.sync.m8n8k4.f64 for every
+// upper block (bi <= bj) of the Gram: the A fragment of group bi and the B
+// fragment of group bj have the same per-lane layout, so each sample is loaded
+// and widened exactly once.  Column sums ride along in the lanes.  Per-CTA
+// partials [B*B + B][G] are summed by region_dmma_merge_kernel.
+constexpr int kRdCons = 256;
+constexpr int kRdP = 512;
+constexpr int kRdStages = 3;
+constexpr int kRdGroups = kMaxBands / 8;     // band groups of 8
+constexpr int kRdEnt = kMaxBands * kMaxBands + kMaxBands;
+
+template <typename T> constexpr int rd_pad() { return 16 / (int)sizeof(T); }  // 16 B: bank spread
+
+template <typename T>
+size_t rd_smem(int bands) {
+  return (size_t)kRdStages * bands * (kRdP + rd_pad<T>()) * sizeof(T) +
+         2 * kRdStages * sizeof(uint64_t) + 128;
+}
+
+struct RdParams {
+  const void* data;   // first pixel of the region (band 0)
+  int64_t bs;
+  int64_t npix;
+  int bands;
+  int G;              // CTAs (= partial records)
+  const double* shift;
+  double* part;       // [kRdEnt][G]
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <typename T, int NG>
+__global__ void __launch_bounds__(kRdCons + 32, 1)
+region_dmma_kernel(RdParams r) {
+  extern __shared__ __align__(128) unsigned char dyn[];
+  __shared__ double red[kRdEnt];
+  __shared__ double shift[kMaxBands];
+  const int B = r.bands;
+  constexpr int PS = kRdP + rd_pad<T>();
+  T* stages = reinterpret_cast<T*>(dyn);
+  uint64_t* full = reinterpret_cast<uint64_t*>(dyn + (size_t)kRdStages * B * PS * sizeof(T));
+  uint64_t* empty = full + kRdStages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < kRdStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kRdCons / 32);
+    }
+    mbar_fence_init();
+  }
+  for (int e = tid; e < kRdEnt; e += blockDim.x) red[e] = 0.0;
+  if (tid < B) shift[tid] = r.shift[tid];
+  __syncthreads();
+  const int64_t ntiles = (r.npix + kRdP - 1) / kRdP;
+  constexpr int NB = NG * (NG + 1) / 2;  // upper 8x8 blocks
+  double c0[NB], c1[NB], dsum[NG];
+#pragma unroll
+  for (int q = 0; q < NB; ++q) c0[q] = c1[q] = 0.0;
+#pragma unroll
+  for (int g = 0; g < NG; ++g) dsum[g] = 0.0;
+  if (warp == kRdCons / 32) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int i = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int st = i % kRdStages;
+        const uint32_t ph = (uint32_t)(i / kRdStages) & 1u;
+        if (i >= kRdStages) mbar_wait(&empty[st], ph ^ 1u);
+        const int64_t p0 = t * kRdP;
+        const int64_t npx = (r.npix - p0) < kRdP ? (r.npix - p0) : kRdP;
+        const uint32_t bytes = (uint32_t)(npx * sizeof(T));
+        mbar_expect_tx(&full[st], bytes * (uint32_t)B);
+        T* dst = stages + (size_t)st * B * PS;
+        const T* src = static_cast<const T*>(r.data) + p0;
+        for (int b = 0; b < B; ++b)
+          bulk_g2s(dst + (size_t)b * PS, src + (int64_t)b * r.bs, bytes, &full[st], pol);
+      }
+    }
+  } else {
+    const int fb = lane >> 2, fp = lane & 3;  // fragment: band 8g + fb, pixel fp of the quad
+    double sh[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) sh[g] = (8 * g + fb < B) ? shift[8 * g + fb] : 0.0;
+    int i = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int st = i % kRdStages;
+      const uint32_t ph = (uint32_t)(i / kRdStages) & 1u;
+      mbar_wait(&full[st], ph);
+      const int64_t p0 = t * kRdP;
+      const int npx = (int)((r.npix - p0) < kRdP ? (r.npix - p0) : kRdP);
+      const T* stage = stages + (size_t)st * B * PS;
+      for (int qd = warp; qd * 4 < npx; qd += kRdCons / 32) {
+        const int px = qd * 4 + fp;
+        double f[NG];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+          const int b = 8 * g + fb;
+          f[g] = (b < B && px < npx) ? widen_f64(stage[(size_t)b * PS + px]) - sh[g] : 0.0;
+          dsum[g] += f[g];
+        }
+        int q = 0;
+#pragma unroll
+        for (int bi = 0; bi < NG; ++bi)
+#pragma unroll
+          for (int bj = bi; bj < NG; ++bj, ++q) dmma(c0[q], c1[q], f[bi], f[bj]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    // fold this warp into the CTA record, one warp at a time (fixed order)
+    for (int w = 0; w < kRdCons / 32; ++w) {
+      if (warp == w) {
+        const int cm = lane >> 2, cn = 2 * (lane & 3);
+        int q = 0;
+#pragma unroll
+        for (int bi = 0; bi < NG; ++bi)
+#pragma unroll
+          for (int bj = bi; bj < NG; ++bj, ++q) {
+            const int row = 8 * bi + cm, col = 8 * bj + cn;
+            if (row < B && col < B) red[row * kMaxBands + col] += c0[q];
+            if (row < B && col + 1 < B) red[row * kMaxBands + col + 1] += c1[q];
+          }
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+          // lanes sharing band 8g + fb differ in fp: sum them (fixed xor tree)
+          double v = dsum[g];
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          if (fp == 0 && 8 * g + fb < B) red[kMaxBands * kMaxBands + 8 * g + fb] += v;
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kRdCons) : "memory");
+    }
+  }
+  __syncthreads();
+  // write the upper triangle (i <= j) + sums as this CTA's partial
+  for (int e = tid; e < kRdEnt; e += blockDim.x) {
+    bool used;
+    if (e < kMaxBands * kMaxBands) {
+      const int ii = e / kMaxBands, jj = e % kMaxBands;
+      used = ii < B && jj < B && (ii >> 3) <= (jj >> 3);
+    } else {
+      used = (e - kMaxBands * kMaxBands) < B;
+    }
+    if (used) r.part[(size_t)e * r.G + blockIdx.x] = red[e];
+  }
+}
+
+// moments = [n, mean, M2]; one warp per output entry, lanes over the G partials.
+__global__ void __launch_bounds__(256)
+region_dmma_merge_kernel(RdParams r, double* __restrict__ moments) {
+  const int B = r.bands, G = r.G;
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int total = 1 + B + B * B;
+  if (e >= total) return;
+  auto sum = [&](int idx) {
+    const double* p = r.part + (size_t)idx * G;
+    double a = 0.0;
+    for (int g = lane; g < G; g += 32) a += p[g];
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    return a;
+  };
+  auto gram = [&](int i, int j) {
+    if ((i >> 3) > (j >> 3)) { const int t = i; i = j; j = t; }
+    return sum(i * kMaxBands + j);
+  };
+  const double n = (double)r.npix;
+  double v;
+  if (e == 0) {
+    v = n;
+  } else if (e <= B) {
+    const int b = e - 1;
+    v = r.shift[b] + sum(kMaxBands * kMaxBands + b) / n;
+  } else {
+    const int q = e - 1 - B, i = q / B, j = q - i * B;
+    const double si = sum(kMaxBands * kMaxBands + i), sj = sum(kMaxBands * kMaxBands + j);
+    v = gram(i, j) - si * sj / n;
+  }
+  if (lane == 0) moments[e] = v;
+}
+
+template <typename T, int NG>
+int launch_region_dmma_ng(RdParams& rp, double* moments, cudaStream_t st) {
+  auto kern = region_dmma_kernel<T, NG>;
+  const size_t smem = rd_smem<T>(rp.bands);
+  static size_t attr = 0;
+  if (attr < smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "region_dmma smem attribute");
+    attr = smem;
+  }
+  kern<<<rp.G, kRdCons + 32, smem, st>>>(rp);
+  UT_CHECK_LAUNCH("region_dmma_kernel");
+  const int total = 1 + rp.bands + rp.bands * rp.bands;
+  region_dmma_merge_kernel<<<(total + 7) / 8, 256, 0, st>>>(rp, moments);
+  UT_CHECK_LAUNCH("region_dmma_merge_kernel");
+  return UT_OK;
+}
+
+template <typename T>
+int launch_region_dmma(const Region& r, RegionWs ws, double* moments, cudaStream_t st) {
+  shift_kernel<T><<<1, 1024, 0, st>>>(r, ws);
+  UT_CHECK_LAUNCH("shift_kernel");
+  RdParams rp;
+  rp.data = static_cast<const T*>(r.data) + r.y0 * r.rs + r.x0;
+  rp.bs = r.bs;
+  rp.npix = r.npix;
+  rp.bands = r.bands;
+  const int64_t ntiles = (r.npix + kRdP - 1) / kRdP;
+  const int64_t g = 148;  // fixed (not the device's SM count): results independent of the GPU
+  rp.G = (int)(ntiles < g ? ntiles : g);
+  rp.shift = ws.shift;
+  rp.part = ws.part;
+  switch ((r.bands + 7) / 8) {
+    case 1: return launch_region_dmma_ng<T, 1>(rp, moments, st);
+    case 2: return launch_region_dmma_ng<T, 2>(rp, moments, st);
+    case 3: return launch_region_dmma_ng<T, 3>(rp, moments, st);
+    default: return launch_region_dmma_ng<T, 4>(rp, moments, st);
+  }
+}
+
+bool region_dmma_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("UT_REGION_DMMA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <typename T>
 int launch_region(Region r, RegionWs ws, double* moments, cudaStream_t st) {
   shift_kernel<T><<<1, 1024, 0, st>>>(r, ws);
@@ -276,6 +519,26 @@ int ut_region_moments(const ut_cube* cube, int64_t x0, int64_t y0, int64_t w, in
   r.tiles_per_cta = (ntiles + G - 1) / G;
   r.G = (int)((ntiles + r.tiles_per_cta - 1) / r.tiles_per_cta);
   cudaStream_t st = as_stream(stream);
+  // whole-width regions of a contiguous cube: TMA + DMMA path
+  const int64_t esz = cube->dtype == UT_U8 ? 1 : (cube->dtype == UT_F64 ? 8 : (cube->dtype == UT_F32 ? 4 : 2));
+  const uintptr_t base = reinterpret_cast<uintptr_t>(cube->data) + (uintptr_t)((y0 * cube->row_stride + x0) * esz);
+  const size_t rd_bytes = cube->dtype == UT_U8 ? rd_smem<uint8_t>(cube->bands)
+                          : cube->dtype == UT_F64 ? rd_smem<double>(cube->bands)
+                          : cube->dtype == UT_F32 ? rd_smem<float>(cube->bands)
+                                                  : rd_smem<uint16_t>(cube->bands);
+  const bool dmma_ok = region_dmma_enabled() && rd_bytes <= 200 * 1024 && x0 == 0 &&
+                       w == cube->cols &&
+                       cube->row_stride == cube->cols && base % 16 == 0 &&
+                       (cube->band_stride * esz) % 16 == 0 && (r.npix * esz) % 16 == 0;
+  if (dmma_ok) {
+    switch (cube->dtype) {
+      case UT_U8: return launch_region_dmma<uint8_t>(r, ws, moments, st);
+      case UT_U16: return launch_region_dmma<uint16_t>(r, ws, moments, st);
+      case UT_F16: return launch_region_dmma<__half>(r, ws, moments, st);
+      case UT_F32: return launch_region_dmma<float>(r, ws, moments, st);
+      case UT_F64: return launch_region_dmma<double>(r, ws, moments, st);
+    }
+  }
   switch (cube->dtype) {
     case UT_U8: return launch_region<uint8_t>(r, ws, moments, st);
     case UT_U16: return launch_region<uint16_t>(r, ws, moments, st);

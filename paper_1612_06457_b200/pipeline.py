@@ -224,5 +224,5 @@ class PcaPipeline(_Sharded):
                                eigenvalues=np.ascontiguousarray(h["evals"][:self.k]))
 
     def launches(self) -> int:
-        """shift + region moments, solve, K4 groups, stretch."""
-        return 2 + 1 + (self.k + 7) // 8 + 1
+        """shift + region moments + merge, solve, K4 groups, stretch."""
+        return 3 + 1 + (self.k + 7) // 8 + 1
