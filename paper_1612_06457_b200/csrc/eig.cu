@@ -41,9 +41,16 @@ __device__ unsigned long long g_eig_phase[32];
       g_eig_phase[(i)] = _t;                                       \
     }                                                              \
   } while (0)
+#define EPV(i, v)                                     \
+  do {                                                \
+    if (threadIdx.x == 0) g_eig_phase[(i)] = (v);     \
+  } while (0)
 #else
 #define EPH(i) \
   do {         \
+  } while (0)
+#define EPV(i, v) \
+  do {            \
   } while (0)
 #endif
 
@@ -147,20 +154,26 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
           // |a_pq| > max(eps/2 sqrt(|a_pp a_qq|), floor), squared (no sqrt)
           const double apq2 = apq * apq;
           if (apq2 > 0.25 * DBL_EPSILON * DBL_EPSILON * fabs(app * aqq) && apq2 > floor2) {
-            // The angle is evaluated in fp32 (short latency chain) on scaled
-            // operands; the rotation is then made orthogonal to fp64 accuracy
-            // and applied as a full similarity, so the angle's precision only
-            // sets how far a_pq drops per step, not the result.
-            const double big = fmax(fabs(aqq - app), 2.0 * fabs(apq));
-            const double sc = 1.0 / big;
-            const float num = (float)((aqq - app) * sc), den = (float)(2.0 * apq * sc);
+            // The angle is evaluated in fp32 with fast intrinsics when the
+            // operands are in range (short latency chain); the rotation is then
+            // made orthogonal to fp64 accuracy and applied as a full
+            // similarity, so the angle's precision only sets how far a_pq drops
+            // per step, not the result.
+            const double dd = aqq - app, d2 = 2.0 * apq;
             double tt;
-            if (fabsf(den) < 1e-18f * fabsf(num)) {
-              tt = apq / (aqq - app);  // theta beyond fp32: t ~ 1 / (2 theta)
-            } else {
-              const float theta = num / den;
-              float tf = 1.0f / (fabsf(theta) + sqrtf(fmaf(theta, theta, 1.0f)));
+            const double mag = fmax(fabs(dd), fabs(d2));
+            if (mag < 1e30 && fabs(d2) > 1e-30 && fabs(d2) > 1e-12 * fabs(dd)) {
+              const float theta = __fdividef((float)dd, (float)d2);
+              const float tf = __frcp_rn(fabsf(theta) + __fsqrt_rn(fmaf(theta, theta, 1.0f)));
               tt = (double)(theta < 0.0f ? -tf : tf);
+            } else {  // out of fp32 range: Rutishauser in fp64
+              const double theta = dd / d2;
+              if (fabs(theta) > 1e150) {
+                tt = 0.5 / theta;
+              } else {
+                tt = 1.0 / (fabs(theta) + sqrt(1.0 + theta * theta));
+                if (theta < 0.0) tt = -tt;
+              }
             }
             const double x = fma(tt, tt, 1.0);
             double rr = (double)rsqrtf((float)x);  // 1/sqrt(1 + t^2): fp32 guess,
@@ -215,7 +228,10 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
     double any = 0.0;
     for (int w = 0; w < NT / 32; ++w) any += s.red[w];
     team_sync<NT>();
-    if (any == 0.0) return 0;
+    if (any == 0.0) {
+      EPV(NT == 32 ? 30 : 31, (unsigned long long)(sweep + 1));
+      return 0;
+    }
   }
   return UT_INFO_NO_CONVERGE;
 }

@@ -27,4 +27,14 @@ for name, h, w in (("cfg1", 512, 512), ("cfg4", 1024, 1024)):
     t = np.array(list(buf), dtype=np.float64)
     t0 = t[0]
     print(cfg.name, [round((t[i] - t0) / 1000, 1) for i in range(11)], "us")
-    print("   sweeps:", [round((t[i] - t0) / 1000, 1) for i in range(11, 31) if t[i] > t0])
+    print("   jacobi sweeps (C x C team32, full team128):", int(t[30]), int(t[31]))
+# full path (general / PCA) sweeps
+import paper_1612_06457_b200.projection as pj  # noqa: E402
+cfg = synthetic.scaled(synthetic.CONFIGS["cfg4pca"], 512, 512)
+stack = synthetic.generate(synthetic.make_scene(cfg))
+for _ in range(2):
+    pm = ut.fit_pca_unsupervised(stack, k=5)
+torch.cuda.synchronize()
+buf = (C.c_ulonglong * 32)()
+f(C.cast(buf, C.c_void_p))
+print("PCA B=32 full Jacobi sweeps:", int(buf[31]))
