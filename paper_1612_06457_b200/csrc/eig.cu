@@ -61,7 +61,7 @@ struct Smem {
   double v[N * LD];   // eigenvectors
   double h[N * LD];   // H, then G = L^-1 H (B x C)
   double cs[N / 2], sn[N / 2], npp[N / 2], nqq[N / 2];
-  int pp[N / 2], qq[N / 2];
+  int pp[N / 2], qq[N / 2], rr[N / 2];
   double red[kThreads / 32];
   double scal[4];
   int flag;
@@ -103,6 +103,15 @@ __device__ bool is_asym(Smem& s, const double* x, int n) {
 
 // Cyclic Jacobi on a (n x n, stride LD) with eigenvectors in v, run by threads
 // [0, NT) of the CTA (the caller parks the others at a __syncthreads).
+#ifdef UT_JACOBI_PROBE
+__device__ long long g_jprobe[8];
+#define JP(i) long long _jp##i = clock64();
+#define JACC(i, a, b) if (t == 0) g_jprobe[i] += (_jp##b - _jp##a);
+#else
+#define JP(i)
+#define JACC(i, a, b)
+#endif
+
 template <int NT>
 __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
   const int t = threadIdx.x;
@@ -132,6 +141,7 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
   for (int sweep = 0; sweep < 40; ++sweep) {
     int rotated = 0;
     for (int r = 0; r < m - 1; ++r) {
+      JP(0)
       // phase A: rotation of pair k (Rutishauser's formulas; round-robin pairs)
       if (t < half) {
         const int k = t;
@@ -185,41 +195,68 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
           }
         }
         s.pp[k] = act ? p : -1;
+        s.rr[k] = p;
         s.qq[k] = q;
         s.cs[k] = c;
         s.sn[k] = sn;
         rotated |= act;
       }
+      JP(1)
       team_sync<NT>();
-      // phase B: rows p, q <- J^T A
-      for (int e = t; e < half * n; e += NT) {
-        const int k = e / n, col = e - k * n;
-        const int p = s.pp[k];
-        if (p >= 0) {
-          const int q = s.qq[k];
-          const double c = s.cs[k], sn = s.sn[k];
-          const double ap = a[p * LD + col], aq = a[q * LD + col];
-          a[p * LD + col] = c * ap - sn * aq;
-          a[q * LD + col] = sn * ap + c * aq;
+      JP(2)
+      // phase B: every 2x2 block (pairs k1, k2) <- J_k1^T A J_k2 in one step
+      // (the blocks partition A, so each thread owns its block), and V <- V J
+      for (int e = t; e < half * half; e += NT) {
+        const int k1 = e / half, k2 = e - k1 * half;
+        const int p1 = s.pp[k1], p2 = s.pp[k2];
+        if (p1 < 0 && p2 < 0) continue;
+        const int q1 = s.qq[k1], q2 = s.qq[k2];
+        if (p1 >= 0 && p2 >= 0) {
+          const double c1 = s.cs[k1], s1 = s.sn[k1], c2 = s.cs[k2], s2 = s.sn[k2];
+          const double x00 = a[p1 * LD + p2], x01 = a[p1 * LD + q2];
+          const double x10 = a[q1 * LD + p2], x11 = a[q1 * LD + q2];
+          const double y00 = c1 * x00 - s1 * x10, y01 = c1 * x01 - s1 * x11;
+          const double y10 = s1 * x00 + c1 * x10, y11 = s1 * x01 + c1 * x11;
+          a[p1 * LD + p2] = c2 * y00 - s2 * y01;
+          a[p1 * LD + q2] = s2 * y00 + c2 * y01;
+          a[q1 * LD + p2] = c2 * y10 - s2 * y11;
+          a[q1 * LD + q2] = s2 * y10 + c2 * y11;
+        } else if (p1 >= 0) {  // rows of pair k1 only; columns of pair k2 (< n)
+          const double c1 = s.cs[k1], s1 = s.sn[k1];
+          for (int side = 0; side < 2; ++side) {
+            const int col = side ? s.qq[k2] : s.rr[k2];
+            if (col >= n) continue;
+            const double x0 = a[p1 * LD + col], x1 = a[q1 * LD + col];
+            a[p1 * LD + col] = c1 * x0 - s1 * x1;
+            a[q1 * LD + col] = s1 * x0 + c1 * x1;
+          }
+        } else {  // columns of pair k2 only
+          const double c2 = s.cs[k2], s2 = s.sn[k2];
+          for (int side = 0; side < 2; ++side) {
+            const int row = side ? s.qq[k1] : s.rr[k1];
+            if (row >= n) continue;
+            const double x0 = a[row * LD + p2], x1 = a[row * LD + q2];
+            a[row * LD + p2] = c2 * x0 - s2 * x1;
+            a[row * LD + q2] = s2 * x0 + c2 * x1;
+          }
         }
       }
-      team_sync<NT>();
-      // phase C: columns p, q <- A J, V <- V J
       for (int e = t; e < half * n; e += NT) {
         const int k = e / n, row = e - k * n;
         const int p = s.pp[k];
         if (p >= 0) {
           const int q = s.qq[k];
           const double c = s.cs[k], sn = s.sn[k];
-          const double ap = a[row * LD + p], aq = a[row * LD + q];
-          a[row * LD + p] = c * ap - sn * aq;
-          a[row * LD + q] = sn * ap + c * aq;
           const double vp = v[row * LD + p], vq = v[row * LD + q];
           v[row * LD + p] = c * vp - sn * vq;
           v[row * LD + q] = sn * vp + c * vq;
         }
       }
+      JP(3) JP(4)
+      JP(5)
       team_sync<NT>();
+      JP(6)
+      JACC(0, 0, 1) JACC(1, 1, 2) JACC(2, 2, 3) JACC(3, 3, 4) JACC(4, 4, 5) JACC(5, 5, 6)
     }
     // any rotation this sweep?  (team-wide OR through shared memory)
     const int warp_any = __any_sync(0xffffffffu, rotated);
