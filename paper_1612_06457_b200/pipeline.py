@@ -48,6 +48,31 @@ class _Sharded:
     def __init__(self, group):
         self.group = group
         self.world = dist.get_world_size(group) if group is not None else 1
+        self.graph = None
+
+    def capture(self):
+        """Record run() as a CUDA graph (single-GPU pipelines): the path is a
+        handful of short kernels at small sizes, so launch overhead matters.
+        Call after one eager run (it sets up workspaces and kernel attributes)."""
+        if self.world > 1:
+            raise RuntimeError("graph capture is for unsharded pipelines")
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.run()  # warm the side stream's workspaces
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            self.run()
+        torch.cuda.synchronize()
+        self.graph = g
+        return g
+
+    def replay(self):
+        self.graph.replay()
+        return self.codes
 
     def gather_moments(self, fit):
         if self.world > 1:

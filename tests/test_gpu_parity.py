@@ -526,3 +526,54 @@ def test_fp64_projector_widening_exact(dtype):
     for got, want in zip(planes, ref):
         rng_ = float(want.max() - want.min())
         assert float(np.abs(got - want).max()) <= 1e-7 * rng_
+
+
+def test_cuda_graph_replay_matches_eager():
+    cfg = _scaled("cfg1", 256, 256, 100)
+    scene = synthetic.make_scene(cfg)
+    stack = synthetic.generate(scene)
+    pipe = ut.CvaPipeline(stack, scene.xs, scene.ys, scene.labels, k=cfg.k)
+    eager = pipe.run().clone()
+    scores = pipe.scores.clone()
+    pipe.capture()
+    pipe.codes.zero_()
+    pipe.scores.zero_()
+    pipe.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(pipe.codes, eager) and torch.equal(pipe.scores, scores)
+    pca = ut.PcaPipeline(stack, k=2)
+    e2 = pca.run().clone()
+    pca.capture()
+    pca.codes.zero_()
+    pca.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(pca.codes, e2)
+
+
+def test_device_stack_api_paths():
+    cfg = _scaled("cfg4", 96, 80, 40)
+    scene = synthetic.make_scene(cfg)
+    stack = synthetic.generate(scene)
+    ts = ut.TrainingSet.from_arrays(scene.xs, scene.ys, scene.labels)
+    dm = ut.assemble_matrix(stack, ts)          # stays in HBM
+    assert dm.on_device
+    model = ut.fit_cva(dm, k=cfg.k)
+    planes = ut.project_stack(stack, model)     # DeviceScorePlanes
+    assert isinstance(planes[0], ut.DeviceScorePlane)
+    host = stack.planes.cpu().numpy()
+    ref = oracle.project(host, {"mean": model.mean, "std": None,
+                                "coefficients": model.coefficients})
+    for p, r in zip(planes, ref):
+        lo, hi = p.range()
+        assert lo == float(p.values.min()) and hi == float(p.values.max())
+        codes = ut.rescale_full(p).cpu().numpy()
+        assert np.array_equal(codes, oracle.rescale_full(p.values.double().cpu().numpy()))
+        assert float(np.abs(p.values.double().cpu().numpy() - r).max()) <= 1e-6 * (r.max() - r.min())
+    hm = ut.fit_cva(ut.assemble_matrix(ut.SpectralStack(stack.bands, host, 8, True), ts),
+                    k=cfg.k)
+    assert np.allclose(hm.coefficients, model.coefficients, atol=1e-12)
+    # fit dispatch
+    m2 = ut.fit("pca_unsupervised", stack=stack, k=2)
+    assert m2.method == "pca_unsupervised" and m2.coefficients.shape == (cfg.bands, 2)
+    with pytest.raises(ut.DataError):
+        ut.fit("nope", dm=dm)
