@@ -426,12 +426,13 @@ project_tma_kernel(ProjParams p, int P, int R) {
 // (<= 8) components of this pass, K = bands, N = pixels.  The A fragments (the
 // weights) stay in registers for the whole kernel; every sample is read from
 // the shared-memory stage and widened to fp64 exactly once (B fragments).  Same
-// producer / 3-stage bulk-copy ring as project_tma_kernel; 8 consumer warps,
-// each owning 64 pixels (8 MMA column groups) of a 512-pixel tile.
+// producer / 3-stage bulk-copy ring as project_tma_kernel; 8 consumer warps
+// per CTA, two CTAs per SM, each warp owning 32 pixels (4 MMA column groups) of
+// a 256-pixel tile (4/8-byte samples).
 constexpr int kDmmaCons = 256;
 // 8-pixel MMA column groups per warp per tile: 64 pixels for 4/8-byte samples,
 // 128 for 1/2-byte samples (keeps each band's bulk copy >= 2 KB)
-template <typename T> constexpr int dmma_groups() { return sizeof(T) >= 4 ? 8 : 16; }
+template <typename T> constexpr int dmma_groups() { return sizeof(T) >= 4 ? 4 : 16; }
 template <typename T> constexpr int dmma_p() { return (kDmmaCons / 32) * dmma_groups<T>() * 8; }
 template <typename T> constexpr int dmma_pad() { return 32 / (int)sizeof(T); }  // 32 B
 
@@ -442,13 +443,13 @@ size_t dmma_smem(int bands) {
 }
 
 __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
 }
 
 template <typename T, int KG>
-__global__ void __launch_bounds__(kDmmaCons + 32, 1)
+__global__ void __launch_bounds__(kDmmaCons + 32, 2)
 project_dmma_kernel(ProjParams p) {
   using Pj = Proj<T, 1, KG, true>;
   __shared__ typename Pj::Smem s;
@@ -575,7 +576,7 @@ int launch_dmma(ProjParams& p, cudaStream_t st) {
     attr = smem;
   }
   const int64_t ntiles = (p.npix + dmma_p<T>() - 1) / dmma_p<T>();
-  int64_t grid = sm_count();
+  int64_t grid = 2 * (int64_t)sm_count();  // two CTAs (2 x 8 consumer warps) per SM
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
   kern<<<(int)grid, kDmmaCons + 32, smem, st>>>(p);
