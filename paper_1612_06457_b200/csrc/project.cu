@@ -443,9 +443,9 @@ size_t dmma_smem(int bands) {
 }
 
 __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-      : "+d"(c0), "+d"(c1)
-      : "d"(a), "d"(b));
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
 }
 
 template <typename T, int KG>
@@ -521,16 +521,21 @@ project_dmma_kernel(ProjParams p) {
       for (int g = 0; g < kDmmaGroups; ++g) c0[g] = c1[g] = 0.0;
       // B fragment: B[k = lane%4][n = lane/4] = x[band 4q + lane%4][pixel n]
       const int bk = lane & 3, bn = lane >> 2;
+      __syncwarp();  // mma.sync.aligned: the whole warp, converged
 #pragma unroll
       for (int q = 0; q < kMaxBands / 4; ++q) {
-        if (q < nq) {
+        if (q < nq) {  // warp-uniform
           const int b = 4 * q + bk;
+          // lanes past the last band read band 0 and zero it without a branch
+          // (a divergent select here could split the warp around the mma)
+          const long long keep = b < B ? -1LL : 0LL;
           const T* row = stage + (size_t)(b < B ? b : 0) * PS + wp0 + bn;
+          double x[kDmmaGroups];
 #pragma unroll
-          for (int g = 0; g < kDmmaGroups; ++g) {
-            const double x = b < B ? widen_f64(row[8 * g]) : 0.0;
-            dmma_884(c0[g], c1[g], afrag[q], x);
-          }
+          for (int g = 0; g < kDmmaGroups; ++g)
+            x[g] = __longlong_as_double(__double_as_longlong(widen_f64(row[8 * g])) & keep);
+#pragma unroll
+          for (int g = 0; g < kDmmaGroups; ++g) dmma_884(c0[g], c1[g], afrag[q], x[g]);
         }
       }
       // C[m = lane/4][n = 2 (lane%4) + {0,1}] -> scores of component m

@@ -326,15 +326,20 @@ region_dmma_kernel(RdParams r) {
       const int64_t p0 = t * kRdP;
       const int npx = (int)((r.npix - p0) < kRdP ? (r.npix - p0) : kRdP);
       const T* stage = stages + (size_t)st * B * PS;
-      for (int qd = warp; qd * 4 < npx; qd += kRdCons / 32) {
+      for (int qd = warp; qd * 4 < npx; qd += kRdCons / 32) {  // warp-uniform
         const int px = qd * 4 + fp;
         double f[NG];
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
           const int b = 8 * g + fb;
-          f[g] = (b < B && px < npx) ? widen_f64(stage[(size_t)b * PS + px]) - sh[g] : 0.0;
+          // branch-free masking keeps the warp converged for mma.sync.aligned
+          const bool ok = b < B && px < npx;
+          const long long keep = ok ? -1LL : 0LL;
+          const double x = widen_f64(stage[(size_t)(ok ? b : 0) * PS + (ok ? px : 0)]) - sh[g];
+          f[g] = __longlong_as_double(__double_as_longlong(x) & keep);
           dsum[g] += f[g];
         }
+        __syncwarp();
         int q = 0;
 #pragma unroll
         for (int bi = 0; bi < NG; ++bi)
