@@ -13,7 +13,7 @@ from .annotations import (AnnotatedPoint, ClassLabel, DesignMatrix, TrainingSet,
 from .eigen import (DEFAULT_RIDGE, EigenSolution, regularize, sign_normalize,  # noqa: F401
                     solve_gen_eig_sym)
 from .errors import DataError, NumericError, UndertextError, UndertextWarning  # noqa: F401
-from .pipeline import CvaPipeline, PcaPipeline, route_points, row_bounds  # noqa: F401
+from .pipeline import CvaPipeline, FolioStream, PcaPipeline, route_points, row_bounds  # noqa: F401
 from .projection import (ALL_METHODS, METHOD_CVA, METHOD_LDA, METHOD_PCA,  # noqa: F401
                          METHOD_PCA_UNSUPERVISED, ProjectionModel, ScatterPair,
                          compute_scatter, fit, fit_cva, fit_pca, fit_pca_unsupervised,

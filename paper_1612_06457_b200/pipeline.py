@@ -138,6 +138,34 @@ class CvaPipeline(_Sharded):
             self.evecs = self.fit.views["evecs"].view(b, b)
             self.mean = self.fit.views["grand_mean"]
 
+    @staticmethod
+    def training_arrays(xs, ys, labels, class_ids=None):
+        """Host-side K1 inputs for an unsharded pipeline: (xy int32 [n,2],
+        class index int32 [n], first point of each class int32 [C]) in K1's
+        class-then-raster order -- precomputed per folio by streaming callers."""
+        xs, ys, labels = (np.asarray(a) for a in (xs, ys, labels))
+        ids, cls = class_index(labels) if class_ids is None else \
+            (class_ids, np.searchsorted(np.asarray(class_ids), labels).astype(np.int32))
+        order = np.lexsort((xs, ys, cls))
+        xy = np.stack([xs[order], ys[order]], axis=1).astype(np.int32)
+        cls = cls[order].astype(np.int32)
+        piv = np.full(len(ids), -1, dtype=np.int32)
+        for c in range(len(ids)):
+            hit = np.flatnonzero(cls == c)
+            if len(hit):
+                piv[c] = hit[0]
+        return xy, cls, piv
+
+    def load_training(self, xy: torch.Tensor, cls: torch.Tensor, pivots: torch.Tensor):
+        """Swap in another training set of the same size (non-blocking copies on
+        the current stream, e.g. from pinned host tensors): streaming folios."""
+        if tuple(xy.shape) != tuple(self.xy.shape) or len(pivots) != len(self.pivots):
+            raise DataError(f"training set shape {tuple(xy.shape)}/{len(pivots)} classes does "
+                            f"not match the pipeline's {tuple(self.xy.shape)}/{len(self.pivots)}")
+        self.xy.copy_(xy, non_blocking=True)
+        self.cls.copy_(cls, non_blocking=True)
+        self.pivots.copy_(pivots, non_blocking=True)
+
     # -- the hot path -------------------------------------------------------
     def fit_only(self):
         self.fit.moments_from_cube(self.cube, self.xy, self.cls, self.n, self.first_bad,
@@ -251,3 +279,66 @@ class PcaPipeline(_Sharded):
     def launches(self) -> int:
         """shift + region moments + merge, solve, K4 groups, stretch."""
         return 3 + 1 + (self.k + 7) // 8 + 1
+
+
+class FolioStream:
+    """A batch of independent folios (each its own cube and training set, same
+    shape) streamed through CVA on one GPU: the next folio's cube and training
+    set are copied host->HBM on a copy stream while the current one is fitted,
+    projected and stretched; its codes are copied back to the host.  Two device
+    buffers ping-pong.  Host tensors should be pinned for the copies to overlap.
+
+    cubes: list of host (B, H, W) tensors; training: list of
+    CvaPipeline.training_arrays() tuples as host tensors; outs: list of host
+    (k, H, W) code tensors the results land in."""
+
+    def __init__(self, cubes, training, outs, k: int, precision: str | None = None,
+                 depth: int = 8, device=None):
+        from .stack import default_bands
+
+        if not cubes:
+            raise DataError("no folios")
+        self.cubes, self.training, self.outs = cubes, training, outs
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        shape = tuple(cubes[0].shape)
+        if any(tuple(c.shape) != shape or c.dtype != cubes[0].dtype for c in cubes):
+            raise DataError("all folios of a stream must share shape and sample type")
+        self.bufs, self.pipes = [], []
+        xy0, cls0, _ = (t.numpy() for t in training[0])
+        for _ in range(2):
+            planes = torch.empty(shape, dtype=cubes[0].dtype, device=self.device)
+            ds = DeviceStack(default_bands(shape[0]), planes, depth, True)
+            # placeholder labels with the same classes; load_training swaps in each folio's
+            self.bufs.append(ds)
+            self.pipes.append(CvaPipeline(ds, xy0[:, 0], xy0[:, 1], cls0, k=k,
+                                          precision=precision, depth=depth))
+        self.copy_stream = torch.cuda.Stream(self.device)
+
+    def launches(self) -> int:
+        return self.pipes[0].launches() * len(self.cubes)
+
+    def run(self):
+        """Enqueue the whole batch on the current stream (+ the copy stream)."""
+        comp = torch.cuda.current_stream(self.device)
+        done = [None, None]
+        for i in range(len(self.cubes)):
+            j = i % 2
+            ready = torch.cuda.Event()
+            with torch.cuda.stream(self.copy_stream):
+                if done[j] is not None:
+                    self.copy_stream.wait_event(done[j])
+                self.bufs[j].planes.copy_(self.cubes[i], non_blocking=True)
+                self.pipes[j].load_training(*self.training[i])
+                ready.record(self.copy_stream)
+            comp.wait_event(ready)
+            self.pipes[j].run()
+            self.outs[i].copy_(self.pipes[j].codes, non_blocking=True)
+            done[j] = torch.cuda.Event()
+            done[j].record(comp)
+        # the copy stream must not run ahead into buffers the caller reuses
+        self.copy_stream.wait_stream(comp)
+
+    def check(self):
+        for p in self.pipes:
+            p.check()

@@ -189,3 +189,33 @@ def test_nonfinite_scores_detected():
     for prec in ("fp64", "fp32"):
         with pytest.raises(ut.DataError, match="NaN"):
             ut.project_stack(ds, m, precision=prec)
+
+
+def test_folio_stream_matches_independent_pipelines():
+    """cfg 5's streaming loop (FolioStream): each folio's codes equal a
+    standalone pipeline's on the same cube and training set."""
+    from dataclasses import replace
+
+    from paper_1612_06457_b200 import synthetic
+
+    base = synthetic.scaled(synthetic.CONFIGS["cfg5"], 200, 160, 60)
+    cubes, train, outs, want = [], [], [], []
+    for f in range(3):
+        sc = synthetic.make_scene(replace(base, seed=77 + f))
+        st = synthetic.generate(sc)
+        cubes.append(st.planes.cpu().pin_memory())
+        arrs = ut.CvaPipeline.training_arrays(sc.xs, sc.ys, sc.labels)
+        train.append(tuple(torch.from_numpy(a).pin_memory() for a in arrs))
+        outs.append(torch.empty((base.k, base.height, base.width), dtype=torch.uint8,
+                                pin_memory=True))
+        ref = ut.CvaPipeline(st, sc.xs, sc.ys, sc.labels, k=base.k)
+        want.append(ref.run().cpu().numpy())
+    fs = ut.FolioStream(cubes, train, outs, k=base.k)
+    for _ in range(2):
+        fs.run()
+        torch.cuda.synchronize()
+        fs.check()
+        for o, w in zip(outs, want):
+            assert np.array_equal(o.numpy(), w)
+    with pytest.raises(ut.DataError):
+        fs.pipes[0].load_training(train[0][0][:5], train[0][1][:5], train[0][2])
