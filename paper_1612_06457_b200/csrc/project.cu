@@ -430,6 +430,10 @@ project_tma_kernel(ProjParams p, int P, int R) {
 // per CTA, two CTAs per SM, each warp owning 32 pixels (4 MMA column groups) of
 // a 256-pixel tile (4/8-byte samples).
 constexpr int kDmmaCons = 256;
+#ifndef UT_DMMA_PROD
+#define UT_DMMA_PROD 2
+#endif
+constexpr int kDmmaProd = UT_DMMA_PROD;  // producer warps: one thread's bulk copies issue ~80 clk apart
 // 8-pixel MMA column groups per warp per tile: 64 pixels for 4/8-byte samples,
 // 128 for 1/2-byte samples (keeps each band's bulk copy >= 2 KB)
 template <typename T> constexpr int dmma_groups() { return sizeof(T) >= 4 ? 4 : 16; }
@@ -449,7 +453,7 @@ __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, doubl
 }
 
 template <typename T, int KG>
-__global__ void __launch_bounds__(kDmmaCons + 32, 2)
+__global__ void __launch_bounds__(kDmmaCons + 32 * kDmmaProd, 2)
 project_dmma_kernel(ProjParams p) {
   using Pj = Proj<T, 1, KG, true>;
   __shared__ typename Pj::Smem s;
@@ -464,7 +468,7 @@ project_dmma_kernel(ProjParams p) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < kTmaStages; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], kDmmaProd);
       mbar_init(&empty[i], kDmmaCons / 32);
     }
     mbar_fence_init();
@@ -477,9 +481,12 @@ project_dmma_kernel(ProjParams p) {
     mn[k] = INFINITY;
     mx[k] = -INFINITY;
   }
-  if (warp == kDmmaCons / 32) {
+  if (warp >= kDmmaCons / 32) {
+    // producers: warp pw issues the rows of bands pw, pw + kDmmaProd, ...
+    const int pw = warp - kDmmaCons / 32;
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
+      const int nb = B > pw ? (B - 1 - pw) / kDmmaProd + 1 : 0;
       int i = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
         const int st = i % kTmaStages;
@@ -488,10 +495,10 @@ project_dmma_kernel(ProjParams p) {
         const int64_t p0 = t * kDmmaP;
         const int64_t npx = (p.npix - p0) < kDmmaP ? (p.npix - p0) : kDmmaP;
         const uint32_t bytes = (uint32_t)(npx * sizeof(T));
-        mbar_expect_tx(&full[st], bytes * (uint32_t)B);
+        mbar_expect_tx(&full[st], bytes * (uint32_t)nb);
         T* dst = stages + (size_t)st * B * PS;
         const T* src = static_cast<const T*>(p.data) + p0;
-        for (int b = 0; b < B; ++b)
+        for (int b = pw; b < B; b += kDmmaProd)
           bulk_g2s(dst + (size_t)b * PS, src + (int64_t)b * p.bs, bytes, &full[st], pol);
       }
     }
@@ -584,7 +591,7 @@ int launch_dmma(ProjParams& p, cudaStream_t st) {
   int64_t grid = 2 * (int64_t)sm_count();  // two CTAs (2 x 8 consumer warps) per SM
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
-  kern<<<(int)grid, kDmmaCons + 32, smem, st>>>(p);
+  kern<<<(int)grid, kDmmaCons + 32 * kDmmaProd, smem, st>>>(p);
   UT_CHECK_LAUNCH("project_dmma_kernel");
   return UT_OK;
 }
