@@ -194,6 +194,23 @@ int ut_plane_minmax(const void* plane, int32_t dtype, int64_t n, double* lohi,
 int ut_linear_to_codes(const void* plane, int32_t dtype, int64_t n, const double* lohi,
                        int32_t depth, void* codes, void* stream);
 
+/* Order statistics for rescale_percentile (rendering.py:146-179): out[j] =
+ * the value of 1-based rank ranks[j] (HOST int64[2]) of the ascending
+ * float32/float64 plane, exact (radix select; no copy of the plane). */
+size_t ut_plane_select_ws(void);
+int ut_plane_select(const void* plane, int32_t dtype, int64_t n, const int64_t* ranks,
+                    double* out, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------- normalize_stack
+ * stack.py:180-213: scope 0 = per-band, 1 = global min/max; out = uint8
+ * planes [bands][rows][cols] contiguous, round_half_away(255 (v - lo) /
+ * (hi - lo)) bit-identical to numpy.  lohi (device, 2*bands doubles) returns
+ * each band's lo, hi; constant[b] = 1 where lo == hi (band -> zeros; the
+ * reference warns).  NaN in a band (scope) gives lo = hi = NaN and zeros. */
+size_t ut_normalize_ws(void);
+int ut_normalize_stack(const ut_cube* cube, int32_t scope, void* out, double* lohi,
+                       int32_t* constant, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------- synthetic cubes
  * Seeded generator for the BASELINE.json configs: class map
  * from `nshapes` shapes (rects kind 0: [y0,x0,y1,x1); ellipses kind 1:

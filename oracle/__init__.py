@@ -27,6 +27,10 @@ from .cva_pca import (  # noqa: F401
     fit_pca_unsupervised,
     gen_eig_sym,
     linear_to_codes,
+    nearest_rank,
+    normalize_stack,
+    rescale_percentile,
+    rescale_training_range,
     project,
     regularize,
     rescale_full,

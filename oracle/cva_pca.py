@@ -17,6 +17,7 @@ Inputs are plain arrays, not the reference's dataclasses:
 
 from __future__ import annotations
 
+import math
 import os
 from concurrent.futures import ThreadPoolExecutor
 
@@ -69,6 +70,63 @@ def rescale_full(plane, depth: int = 8) -> np.ndarray:
     if lo == hi:
         return np.zeros(p.shape, dtype=np.uint8 if depth == 8 else np.uint16)
     return linear_to_codes(p, lo, hi, depth)
+
+
+def rescale_training_range(plane, training_scores, k: int, depth: int = 8) -> np.ndarray:
+    """rendering.py:133-152 -- window = span of component k's training scores."""
+    row = np.asarray(training_scores)[k]
+    lo, hi = float(row.min()), float(row.max())
+    p = np.asarray(plane, dtype=np.float64)
+    if lo == hi:
+        return np.zeros(p.shape, dtype=np.uint8 if depth == 8 else np.uint16)
+    return linear_to_codes(p, lo, hi, depth)
+
+
+def nearest_rank(sorted_values, p: float) -> float:
+    """rendering.py:146-152 -- element ceil(p/100 n) of the ascending sample."""
+    n = len(sorted_values)
+    rank = max(1, math.ceil(p / 100.0 * n))
+    return float(sorted_values[rank - 1])
+
+
+def rescale_percentile(plane, p: float, depth: int = 8, one_tail: bool = False) -> np.ndarray:
+    """rendering.py:155-179 -- nearest-rank window [p, 100-p] (or [min, 100-p])."""
+    v = np.asarray(plane, dtype=np.float64)
+    flat = np.sort(v, axis=None)
+    lo = float(flat[0]) if one_tail else nearest_rank(flat, p)
+    hi = nearest_rank(flat, 100.0 - p)
+    if lo == hi:
+        return np.zeros(v.shape, dtype=np.uint8 if depth == 8 else np.uint16)
+    return linear_to_codes(v, lo, hi, depth)
+
+
+# --------------------------------------------------------------------------
+# stack.py
+# --------------------------------------------------------------------------
+
+def normalize_stack(planes, scope: str = "per-band"):
+    """stack.py:180-213 -- (codes uint8, constant-band flags).
+
+    lo/hi per band (or over the cube); 255 * (v - lo) / (hi - lo) in float64,
+    rounded half away; a constant band maps to zeros (the reference warns).
+    """
+    planes = np.asarray(planes)
+    out = np.empty(planes.shape, dtype=np.uint8)
+    flags = np.zeros(planes.shape[0], dtype=bool)
+    if scope == "global":
+        lo, hi = float(planes.min()), float(planes.max())
+    for i in range(planes.shape[0]):
+        plane = planes[i]
+        if scope == "per-band":
+            lo, hi = float(plane.min()), float(plane.max())
+        if lo == hi:
+            flags[i] = True
+            out[i] = 0
+            continue
+        scaled = 255.0 * (plane.astype(np.float64) - lo) / (hi - lo)
+        with np.errstate(invalid="ignore"):
+            out[i] = round_half_away(scaled).astype(np.uint8)
+    return out, flags
 
 
 # --------------------------------------------------------------------------

@@ -19,7 +19,9 @@ from .projection import (ALL_METHODS, METHOD_CVA, METHOD_LDA, METHOD_PCA,  # noq
                          compute_scatter, fit, fit_cva, fit_pca, fit_pca_unsupervised,
                          project_stack)
 from .quantize import code_dtype, linear_to_codes, max_code, round_half_away  # noqa: F401
-from .rendering import DeviceScorePlane, ScorePlane, rescale_full  # noqa: F401
-from .stack import BandMeta, DeviceStack, SpectralStack  # noqa: F401
+from .rendering import (PERCENTILE_CHOICES, DeviceScorePlane, RenderSpec,  # noqa: F401
+                        ScorePlane, nearest_rank_percentile, rescale, rescale_full,
+                        rescale_percentile, rescale_training_range)
+from .stack import BandMeta, DeviceStack, SpectralStack, normalize_stack  # noqa: F401
 
 __version__ = "0.1.0"

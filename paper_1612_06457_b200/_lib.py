@@ -26,6 +26,7 @@ EXPORTS = (
     "ut_class_moments", "ut_cube_class_moments", "ut_cva_solve", "ut_gen_eig_sym", "ut_region_moments_ws",
     "ut_region_moments", "ut_pca_solve", "ut_project_ws", "ut_project_minmax",
     "ut_stretch", "ut_plane_minmax_ws", "ut_plane_minmax", "ut_linear_to_codes",
+    "ut_plane_select_ws", "ut_plane_select", "ut_normalize_ws", "ut_normalize_stack",
     "ut_synth_cube", "ut_class_of",
 )
 
@@ -70,6 +71,10 @@ _SIGS = {
     "ut_plane_minmax_ws": (SZ, []),
     "ut_plane_minmax": (I32, [P, I32, I64, P, P, P, SZ, P]),
     "ut_linear_to_codes": (I32, [P, I32, I64, P, I32, P, P]),
+    "ut_plane_select_ws": (SZ, []),
+    "ut_plane_select": (I32, [P, I32, I64, P, P, P, SZ, P]),
+    "ut_normalize_ws": (SZ, []),
+    "ut_normalize_stack": (I32, [C.POINTER(Cube), I32, P, P, P, P, SZ, P]),
     "ut_synth_cube": (I32, [C.POINTER(Cube), I64, P, P, I32, P, I32, C.c_uint64, P]),
     "ut_class_of": (I32, [P, I32, P, I64, P, P]),
 }

@@ -6,11 +6,15 @@ ScorePlane (float64 numpy, finite-checked) is rescaled on the device by
 ``ut_plane_minmax`` + ``ut_linear_to_codes``; a ``DeviceScorePlane`` (one fp32
 plane of the projector's output, with the min/max the projector already
 reduced) is rescaled by ``ut_stretch`` without another reduction pass.
-The other rescale modes, composites and codecs are outside the hot path.
+The training-range and percentile modes (:133-179) use the same
+``ut_linear_to_codes``; the percentile window comes from an exact radix select
+on the device (``ut_plane_select``).  Composites and codecs are outside the path.
 """
 
 from __future__ import annotations
 
+import ctypes as C
+import math
 import warnings
 from dataclasses import dataclass, field
 
@@ -21,6 +25,43 @@ from . import _lib
 from . import device as dev
 from .errors import DataError, UndertextWarning
 from .quantize import _torch_code_dtype, code_dtype, max_code
+
+
+MODE_FULL_RANGE = "full"            # rendering.py:31-36
+MODE_TRAINING_RANGE = "training"
+MODE_PERCENTILE = "percentile"
+RESCALE_MODES = (MODE_FULL_RANGE, MODE_TRAINING_RANGE, MODE_PERCENTILE)
+PERCENTILE_CHOICES = (0.01, 0.1, 1.0, 5.0)
+
+
+@dataclass(frozen=True)
+class RenderSpec:
+    """How to quantize score planes: mode, optional percentile, bit depth
+    (rendering.py:63-93)."""
+
+    mode: str = MODE_FULL_RANGE
+    percentile_p: float | None = None
+    out_depth: int = 8
+    one_tail: bool = False
+
+    def __post_init__(self):
+        if self.mode not in RESCALE_MODES:
+            raise DataError(f"unknown rescale mode {self.mode!r}")
+        if self.out_depth not in (8, 16):
+            raise DataError(f"bit depth must be 8 or 16, got {self.out_depth}")
+        if self.mode == MODE_PERCENTILE:
+            if self.percentile_p not in PERCENTILE_CHOICES:
+                raise DataError(f"percentile must be one of {PERCENTILE_CHOICES}, "
+                                f"got {self.percentile_p!r}")
+        elif self.percentile_p is not None:
+            raise DataError(f"percentile given but mode is {self.mode!r}")
+
+    def suffix(self) -> str:
+        if self.mode == MODE_PERCENTILE:
+            p = self.percentile_p
+            text = str(int(p)) if float(p).is_integer() else str(p).replace(".", "_")
+            return f"_p{text}"
+        return f"_{self.mode}"
 
 
 @dataclass(frozen=True)
@@ -132,3 +173,95 @@ def rescale_full(plane, depth: int = 8):
         _zeros_warning("constant score plane")
         return np.zeros(v.shape, dtype=code_dtype(depth))
     return host
+
+
+# ---------------------------------------------------------------- other modes
+
+def _plane_on_device(plane):
+    """(values tensor on the device, UT dtype, shape, is_host) of a plane."""
+    if isinstance(plane, DeviceScorePlane):
+        v = plane.values
+        if not v.is_contiguous():
+            v = v.contiguous()
+        return v, dev.TORCH_TO_UT[v.dtype], tuple(v.shape), False
+    if not isinstance(plane, ScorePlane):
+        plane = ScorePlane(plane)
+    device = dev.require_cuda()
+    v = dev.to_device(plane.values, device)
+    return v, _lib.UT_F64, plane.values.shape, True
+
+
+def _codes(v, dtype, shape, lohi, depth, host):
+    codes = torch.empty(int(np.prod(shape)), dtype=_torch_code_dtype(depth), device=v.device)
+    _lib.check(_lib.lib().ut_linear_to_codes(v.data_ptr(), dtype, codes.numel(), lohi.data_ptr(),
+                                             depth, codes.data_ptr(), dev.stream_handle()),
+               "ut_linear_to_codes")
+    codes = codes.view(shape)
+    return codes.cpu().numpy() if host else codes
+
+
+def _zeros(shape, depth, host, device):
+    if host:
+        return np.zeros(shape, dtype=code_dtype(depth))
+    return torch.zeros(shape, dtype=_torch_code_dtype(depth), device=device)
+
+
+def rescale_training_range(plane, model, k: int, depth: int = 8):
+    """Map the training-score span of component k onto the code range
+    (rendering.py:133-152); values outside clamp to 0 / the top code."""
+    if model.training_scores is None:
+        raise DataError("model has no training scores (unsupervised fit); use full-range")
+    if not (0 <= k < model.training_scores.shape[0]):
+        raise DataError(f"component {k} out of range")
+    max_code(depth)
+    row = model.training_scores[k]
+    lo, hi = float(row.min()), float(row.max())
+    v, dtype, shape, host = _plane_on_device(plane)
+    if lo == hi:
+        _zeros_warning(f"training scores constant for component {k}")
+        return _zeros(shape, depth, host, v.device)
+    lohi = torch.tensor([lo, hi], dtype=torch.float64).to(v.device)
+    return _codes(v, dtype, shape, lohi, depth, host)
+
+
+def nearest_rank_percentile(sorted_values, p: float) -> float:
+    """Element ceil(p/100 n) (1-based) of an ascending sample
+    (rendering.py:146-152; host helper, as in the reference)."""
+    n = len(sorted_values)
+    rank = max(1, math.ceil(p / 100.0 * n))
+    return float(sorted_values[rank - 1])
+
+
+def rescale_percentile(plane, p: float, depth: int = 8, one_tail: bool = False):
+    """Clip the darkest and brightest p percent, then map linearly
+    (rendering.py:155-179).  lo / hi are the nearest-rank p-th and (100-p)-th
+    percentiles, found on the device by an exact radix select."""
+    if p not in PERCENTILE_CHOICES:
+        raise DataError(f"percentile must be one of {PERCENTILE_CHOICES}, got {p!r}")
+    max_code(depth)
+    v, dtype, shape, host = _plane_on_device(plane)
+    n = int(np.prod(shape))
+    r_lo = 1 if one_tail else max(1, math.ceil(p / 100.0 * n))
+    r_hi = max(1, math.ceil((100.0 - p) / 100.0 * n))
+    ranks = (C.c_int64 * 2)(r_lo, r_hi)
+    lohi = torch.empty(2, dtype=torch.float64, device=v.device)
+    L = _lib.lib()
+    ws = dev.workspace("plane_select", L.ut_plane_select_ws(), v.device)
+    _lib.check(L.ut_plane_select(v.data_ptr(), dtype, n, ranks, lohi.data_ptr(), ws.data_ptr(),
+                                 ws.numel(), dev.stream_handle()), "ut_plane_select")
+    lo, hi = lohi.cpu().numpy()
+    if lo == hi:
+        _zeros_warning(f"percentile window empty at p={p}")
+        return _zeros(shape, depth, host, v.device)
+    return _codes(v, dtype, shape, lohi, depth, host)
+
+
+def rescale(plane, spec: RenderSpec, model=None, k: int | None = None):
+    """Apply the rescale mode named by ``spec`` to one plane (rendering.py:182-195)."""
+    if spec.mode == MODE_FULL_RANGE:
+        return rescale_full(plane, spec.out_depth)
+    if spec.mode == MODE_TRAINING_RANGE:
+        if model is None or k is None:
+            raise DataError("training-range rescale needs the fitted model and plane index")
+        return rescale_training_range(plane, model, k, spec.out_depth)
+    return rescale_percentile(plane, spec.percentile_p, spec.out_depth, spec.one_tail)

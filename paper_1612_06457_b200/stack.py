@@ -12,6 +12,7 @@ sequence -- assemble_matrix, fit, project_stack on one stack -- pays one H2D.
 
 from __future__ import annotations
 
+import ctypes as C
 import threading
 import weakref
 from dataclasses import dataclass, field
@@ -165,3 +166,48 @@ def _weakrefable(a) -> bool:
         return True
     except TypeError:
         return False
+
+
+def normalize_stack(stack, scope: str = "per-band"):
+    """Min-max map samples onto [0, 255], rounded ties away (stack.py:180-213).
+
+    ``scope="per-band"`` maps each band by its own min/max, ``"global"`` by the
+    cube's.  A constant band (stack) maps to zeros with a warning; an already
+    normalized stack is refused.  Host SpectralStack -> host SpectralStack
+    (uint8, normalized); DeviceStack -> DeviceStack in HBM.  Both passes run on
+    the GPU (``ut_normalize_stack``); codes are bit-identical to numpy's.
+    """
+    import warnings
+
+    from . import _lib
+    from .errors import UndertextWarning
+
+    if not isinstance(stack, (SpectralStack, DeviceStack)):
+        raise DataError(f"expected a SpectralStack or DeviceStack, got {type(stack).__name__}")
+    if stack.normalized:
+        raise DataError("stack is already normalized")
+    if scope not in ("per-band", "global"):
+        raise DataError(f"unknown normalization scope {scope!r}")
+    host = isinstance(stack, SpectralStack)
+    ds = DeviceStack.from_host(stack) if host else stack
+    device = ds.planes.device
+    b = ds.band_count
+    with torch.cuda.device(device):
+        out = torch.empty((b, ds.height, ds.width), dtype=torch.uint8, device=device)
+        lohi = torch.empty(2 * b, dtype=torch.float64, device=device)
+        const = torch.empty(b, dtype=torch.int32, device=device)
+        L = _lib.lib()
+        ws = dev.workspace("normalize", L.ut_normalize_ws(), device)
+        cube = ds.cube()
+        _lib.check(L.ut_normalize_stack(C.byref(cube), 0 if scope == "per-band" else 1,
+                                        out.data_ptr(), lohi.data_ptr(), const.data_ptr(),
+                                        ws.data_ptr(), ws.numel(), dev.stream_handle()),
+                   "ut_normalize_stack")
+        flags = const.cpu().numpy()
+        lo = lohi.cpu().numpy()[0::2]
+    for i in np.flatnonzero(flags):
+        warnings.warn(f"band {ds.bands[i].band_id} is constant (value {int(lo[i])}); "
+                      f"normalized to all zeros", UndertextWarning, stacklevel=2)
+    if host:
+        return SpectralStack(stack.bands, out.cpu().numpy(), 8, normalized=True)
+    return DeviceStack(ds.bands, out, 8, True, ds.row0, ds.full_height)

@@ -34,7 +34,9 @@ from undertext.eigen import solve_gen_eig_sym  # noqa: E402
 from undertext.projection import (  # noqa: E402
     compute_scatter, fit_cva, fit_pca_unsupervised, project_stack,
 )
-from undertext.rendering import ScorePlane, rescale_full  # noqa: E402
+from undertext.projection import ProjectionModel  # noqa: E402
+from undertext.rendering import (ScorePlane, rescale_full, rescale_percentile,  # noqa: E402
+                                 rescale_training_range)
 from undertext.stack import BandMeta, SpectralStack, normalize_stack  # noqa: E402
 from undertext.synthetic import make_palimpsest  # noqa: E402
 
@@ -161,6 +163,56 @@ def rescale_cases():
     np.savez_compressed(HERE / "rescale.npz", **out)
 
 
+def normalize_cases():
+    """stack.py:180-213 on raw (not normalized) stacks of every sample type."""
+    rng = np.random.default_rng(9)
+    cases = {
+        "u8": (rng.integers(3, 220, size=(3, 17, 23)).astype(np.uint8), 8),
+        "u16": (rng.integers(100, 4000, size=(4, 16, 20)).astype(np.uint16), 16),
+        "u16_span": (np.array([[[0, 32768, 65535]]], dtype=np.uint16), 16),
+        "f32": (rng.uniform(0, 200, size=(2, 12, 15)).astype(np.float32), 8),
+        "f64_ties": (np.array([[[0.0, 0.5, 1.0, 127.0, 255.0, 2.0, 254.0]]]), 8),
+        "const": (np.stack([np.full((4, 5), 7, np.uint8),
+                            rng.integers(0, 9, size=(4, 5)).astype(np.uint8)]), 8),
+    }
+    out = {}
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for key, (planes, depth) in cases.items():
+            metas = tuple(BandMeta(i, 400.0 + i, "x") for i in range(planes.shape[0]))
+            st = SpectralStack(metas, planes, depth)
+            out[f"{key}_in"] = planes
+            out[f"{key}_depth"] = np.array(depth)
+            for scope in ("per-band", "global"):
+                out[f"{key}_{scope}"] = normalize_stack(st, scope=scope).planes
+    np.savez_compressed(HERE / "normalize.npz", **out)
+
+
+def rescale_mode_cases():
+    """rendering.py:133-179: training-range and percentile windows."""
+    rng = np.random.default_rng(10)
+    out = {}
+    plane = rng.normal(size=(37, 41))
+    out["plane"] = plane
+    scores = rng.normal(scale=0.8, size=(3, 50))
+    model = ProjectionModel(method="cva", mean=np.zeros(2), std=None,
+                            coefficients=np.ones((2, 3)), eigenvalues=np.ones(3),
+                            training_scores=scores)
+    out["training_scores"] = scores
+    for k in range(3):
+        out[f"train_k{k}_u8"] = rescale_training_range(ScorePlane(plane), model, k)
+        out[f"train_k{k}_u16"] = rescale_training_range(ScorePlane(plane), model, k, depth=16)
+    for p in (0.01, 0.1, 1.0, 5.0):
+        tag = str(p).replace(".", "_")
+        out[f"pct_{tag}"] = rescale_percentile(ScorePlane(plane), p)
+        out[f"pct_{tag}_one"] = rescale_percentile(ScorePlane(plane), p, one_tail=True)
+        out[f"pct_{tag}_u16"] = rescale_percentile(ScorePlane(plane), p, depth=16)
+    lin = rng.permutation(np.linspace(0.0, 1.0, 1000)).reshape(25, 40)
+    out["lin"] = lin
+    out["lin_p5"] = rescale_percentile(ScorePlane(lin), 5.0)
+    np.savez_compressed(HERE / "rescale_modes.npz", **out)
+
+
 if __name__ == "__main__":
     scatter_cases()
     eigen_cases()
@@ -171,5 +223,7 @@ if __name__ == "__main__":
     cube_case("cva_f32_b32", 40, 40, 32, 6, np.float32, 15, 40, 5, 8, per_class_cov=True)
     small_page_case()
     rescale_cases()
+    normalize_cases()
+    rescale_mode_cases()
     for p in sorted(HERE.glob("*.npz")):
         print(p.name, p.stat().st_size)

@@ -130,3 +130,46 @@ def test_pca_equal_bands_rank_one():
     pm = oracle.fit_pca_unsupervised(np.stack([plane, plane, plane]))
     assert pm["eigenvalues"][0] == pytest.approx(3.0, rel=1e-8)
     assert np.allclose(pm["eigenvalues"][1:], 0.0, atol=1e-9)
+
+
+NORMALIZE_CASES = ["u8", "u16", "u16_span", "f32", "f64_ties", "const"]
+
+
+@pytest.mark.parametrize("key", NORMALIZE_CASES)
+@pytest.mark.parametrize("scope", ["per-band", "global"])
+def test_normalize_golden(key, scope):
+    """stack.py:180-213 restated: bit-identical codes on every sample type."""
+    g = load("normalize")
+    codes, _ = oracle.normalize_stack(g[f"{key}_in"], scope)
+    assert np.array_equal(codes, g[f"{key}_{scope}"])
+
+
+def test_normalize_known_answers():
+    # tests/test_stack.py:113-154 of the reference, restated
+    codes, _ = oracle.normalize_stack(np.array([[[0, 32768, 65535]]], dtype=np.uint16))
+    assert codes[0].tolist() == [[0, 128, 255]]
+    ident = np.arange(256, dtype=np.uint8).reshape(1, 16, 16)
+    assert np.array_equal(oracle.normalize_stack(ident)[0], ident)
+    two = np.stack([np.array([[0, 50]], np.uint8), np.array([[50, 100]], np.uint8)])
+    g, _ = oracle.normalize_stack(two, "global")
+    assert g[0].tolist() == [[0, 128]] and g[1].tolist() == [[128, 255]]
+    c, flags = oracle.normalize_stack(np.full((1, 2, 2), 7, np.uint8))
+    assert c.max() == 0 and flags.tolist() == [True]
+
+
+def test_rescale_modes_golden():
+    """rendering.py:133-179 restated: training-range and percentile windows."""
+    g = load("rescale_modes")
+    plane, scores = g["plane"], g["training_scores"]
+    for k in range(3):
+        assert np.array_equal(oracle.rescale_training_range(plane, scores, k), g[f"train_k{k}_u8"])
+        assert np.array_equal(oracle.rescale_training_range(plane, scores, k, 16),
+                              g[f"train_k{k}_u16"])
+    for p in (0.01, 0.1, 1.0, 5.0):
+        tag = str(p).replace(".", "_")
+        assert np.array_equal(oracle.rescale_percentile(plane, p), g[f"pct_{tag}"])
+        assert np.array_equal(oracle.rescale_percentile(plane, p, one_tail=True), g[f"pct_{tag}_one"])
+        assert np.array_equal(oracle.rescale_percentile(plane, p, 16), g[f"pct_{tag}_u16"])
+    assert np.array_equal(oracle.rescale_percentile(g["lin"], 5.0), g["lin_p5"])
+    flat = np.sort(np.random.default_rng(1).normal(size=1000))
+    assert oracle.nearest_rank(flat, 1.0) == flat[9] and oracle.nearest_rank(flat, 99.0) == flat[989]
