@@ -53,31 +53,90 @@ __global__ void norm_init_kernel(NormWs ws) {
   }
 }
 
+// min/max in the sample's own arithmetic (integers / float; exact), NaN-aware
+template <typename T> struct MinMax {
+  using A = float;
+  __device__ static A lo0() { return INFINITY; }
+  __device__ static A hi0() { return -INFINITY; }
+  __device__ static A of(T x) { return to_f32(x); }
+  __device__ static bool nan(A a) { return a != a; }
+  __device__ static A mn(A a, A b) { return fminf(a, b); }
+  __device__ static A mx(A a, A b) { return fmaxf(a, b); }
+};
+template <> struct MinMax<uint8_t> {
+  using A = unsigned;
+  __device__ static A lo0() { return 0xffffffffu; }
+  __device__ static A hi0() { return 0u; }
+  __device__ static A of(uint8_t x) { return x; }
+  __device__ static bool nan(A) { return false; }
+  __device__ static A mn(A a, A b) { return min(a, b); }
+  __device__ static A mx(A a, A b) { return max(a, b); }
+};
+template <> struct MinMax<uint16_t> : MinMax<uint8_t> {
+  __device__ static A of(uint16_t x) { return x; }
+};
+template <> struct MinMax<double> {
+  using A = double;
+  __device__ static A lo0() { return INFINITY; }
+  __device__ static A hi0() { return -INFINITY; }
+  __device__ static A of(double x) { return x; }
+  __device__ static bool nan(A a) { return a != a; }
+  __device__ static A mn(A a, A b) { return fmin(a, b); }
+  __device__ static A mx(A a, A b) { return fmax(a, b); }
+};
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
 norm_minmax_kernel(ut_cube c, NormWs ws) {
+  using M = MinMax<T>;
+  using A = typename M::A;
   const int b = blockIdx.y;
   const T* base = static_cast<const T*>(c.data) + (int64_t)b * c.band_stride;
   const int64_t n = c.rows * c.cols;
-  double mn = INFINITY, mx = -INFINITY;
+  A mn = M::lo0(), mx = M::hi0();
   bool nan = false;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / c.cols, col = i - r * c.cols;
-    const double x = to_f64(base[r * c.row_stride + col]);
-    nan |= (x != x);
-    mn = fmin(mn, x);
-    mx = fmax(mx, x);
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (c.row_stride == c.cols && (reinterpret_cast<uintptr_t>(base) % 16) == 0) {
+    constexpr int V = 16 / sizeof(T);
+    const int64_t nv = n / V;
+    for (int64_t i = tid; i < nv; i += stride) {
+      T x[V];
+      *reinterpret_cast<uint4*>(x) = ld_stream_u4(base + V * i);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const A a = M::of(x[j]);
+        nan |= M::nan(a);
+        mn = M::mn(mn, a);
+        mx = M::mx(mx, a);
+      }
+    }
+    for (int64_t i = nv * V + tid; i < n; i += stride) {
+      const A a = M::of(base[i]);
+      nan |= M::nan(a);
+      mn = M::mn(mn, a);
+      mx = M::mx(mx, a);
+    }
+  } else {
+    for (int64_t r = blockIdx.x; r < c.rows; r += gridDim.x)  // a block per row
+      for (int64_t col = threadIdx.x; col < c.cols; col += blockDim.x) {
+        const A a = M::of(base[r * c.row_stride + col]);
+        nan |= M::nan(a);
+        mn = M::mn(mn, a);
+        mx = M::mx(mx, a);
+      }
   }
+  double dmn = (double)mn, dmx = (double)mx;
+  if (!(mn <= mx)) { dmn = INFINITY; dmx = -INFINITY; }  // nothing seen (or only NaN)
   for (int o = 16; o > 0; o >>= 1) {
-    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+    dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
   }
   nan = __any_sync(0xffffffffu, nan);
   if ((threadIdx.x & 31) == 0) {
-    if (mn <= mx) {  // the warp saw at least one non-NaN sample
-      atomicMin(&ws.mn[b], order_key(mn));
-      atomicMax(&ws.mx[b], order_key(mx));
+    if (dmn <= dmx) {
+      atomicMin(&ws.mn[b], order_key(dmn));
+      atomicMax(&ws.mx[b], order_key(dmx));
     }
     if (nan) atomicOr(&ws.nan[b], 1);
   }
@@ -119,6 +178,63 @@ __device__ __forceinline__ uint8_t norm_code(double v, double lo, double den, do
   return (code >= 0.0 && code <= 255.0) ? (uint8_t)(int)code : (uint8_t)0;
 }
 
+// exact widening: the ALU bit trick for normal floats (F2F is quarter rate),
+// the conversion instruction for zeros / subnormals (rare: a branch)
+template <typename T>
+__device__ __forceinline__ double norm_in(T x) { return to_f64(x); }
+template <> __device__ __forceinline__ double norm_in<float>(float x) {
+  if ((__float_as_uint(x) & 0x7f800000u) == 0u) return (double)x;
+  return widen_f64(x);
+}
+template <> __device__ __forceinline__ double norm_in<__half>(__half x) {
+  return norm_in<float>(__half2float(x));
+}
+
+// 8/16-bit samples: the code depends on the sample value only -> a per-block
+// table over [lo, hi] in shared memory, built with the exact arithmetic, then
+// one table lookup per sample.
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+norm_codes_lut_kernel(ut_cube c, const double* __restrict__ lohi, uint8_t* __restrict__ out) {
+  extern __shared__ uint8_t lut[];
+  const int b = blockIdx.y;
+  const double lo = lohi[2 * b], hi = lohi[2 * b + 1];
+  const T* base = static_cast<const T*>(c.data) + (int64_t)b * c.band_stride;
+  const int64_t n = c.rows * c.cols;
+  uint8_t* o = out + (int64_t)b * n;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (!(lo < hi)) {  // constant band -> zeros
+    for (int64_t i = tid; i < n; i += stride) o[i] = 0;
+    return;
+  }
+  const int ilo = (int)lo, range = (int)hi - ilo + 1;
+  const double den = __dadd_rn(hi, -lo), rden = __drcp_rn(den);
+  for (int j = threadIdx.x; j < range; j += blockDim.x) lut[j] = norm_code((double)(ilo + j), lo, den, rden);
+  __syncthreads();
+  if (c.row_stride == c.cols && (reinterpret_cast<uintptr_t>(base) % 16) == 0 &&
+      (reinterpret_cast<uintptr_t>(o) % 16) == 0) {
+    constexpr int V = 16 / sizeof(T);  // samples per 16-byte load
+    const int64_t nv = n / 16;
+    for (int64_t i = tid; i < nv; i += stride) {
+      T x[16];
+#pragma unroll
+      for (int q = 0; q < 16 / V; ++q) *reinterpret_cast<uint4*>(x + q * V) = ld_stream_u4(base + 16 * i + q * V);
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        w[q] = (uint32_t)lut[(int)x[4 * q] - ilo] | ((uint32_t)lut[(int)x[4 * q + 1] - ilo] << 8) |
+               ((uint32_t)lut[(int)x[4 * q + 2] - ilo] << 16) | ((uint32_t)lut[(int)x[4 * q + 3] - ilo] << 24);
+      st_stream_u4(o + 16 * i, make_uint4(w[0], w[1], w[2], w[3]));
+    }
+    for (int64_t i = nv * 16 + tid; i < n; i += stride) o[i] = lut[(int)base[i] - ilo];
+    return;
+  }
+  for (int64_t r = blockIdx.x; r < c.rows; r += gridDim.x)
+    for (int64_t col = threadIdx.x; col < c.cols; col += blockDim.x)
+      o[r * c.cols + col] = lut[(int)base[r * c.row_stride + col] - ilo];
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
 norm_codes_kernel(ut_cube c, const double* __restrict__ lohi, uint8_t* __restrict__ out) {
@@ -127,20 +243,20 @@ norm_codes_kernel(ut_cube c, const double* __restrict__ lohi, uint8_t* __restric
   const T* base = static_cast<const T*>(c.data) + (int64_t)b * c.band_stride;
   const int64_t n = c.rows * c.cols;
   uint8_t* o = out + (int64_t)b * n;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (!(lo != hi)) {  // constant band: zeros (NaN bands fall through: codes 0 below)
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-      o[i] = 0;
+    for (int64_t i = tid; i < n; i += stride) o[i] = 0;
     return;
   }
   const double den = __dadd_rn(hi, -lo);
   const double rden = __drcp_rn(den);
-  if (c.row_stride == c.cols && (reinterpret_cast<uintptr_t>(base) % 16) == 0 && n % 16 == 0) {
+  if (c.row_stride == c.cols && (reinterpret_cast<uintptr_t>(base) % 16) == 0 &&
+      (reinterpret_cast<uintptr_t>(o) % 16) == 0) {
     // contiguous band: 16 samples per thread-iteration, one 16-byte store
     constexpr int V = 16 / sizeof(T);
-    const int64_t n16 = n / 16;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nv = n / 16;
+    for (int64_t i = tid; i < nv; i += stride) {
       T x[16];
 #pragma unroll
       for (int q = 0; q < 16 / V; ++q)
@@ -150,18 +266,17 @@ norm_codes_kernel(ut_cube c, const double* __restrict__ lohi, uint8_t* __restric
       for (int q = 0; q < 4; ++q) {
         uint32_t acc = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc |= (uint32_t)norm_code(to_f64(x[4 * q + j]), lo, den, rden) << (8 * j);
+        for (int j = 0; j < 4; ++j) acc |= (uint32_t)norm_code(norm_in(x[4 * q + j]), lo, den, rden) << (8 * j);
         w[q] = acc;
       }
       st_stream_u4(o + 16 * i, make_uint4(w[0], w[1], w[2], w[3]));
     }
+    for (int64_t i = nv * 16 + tid; i < n; i += stride) o[i] = norm_code(to_f64(base[i]), lo, den, rden);
     return;
   }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / c.cols, col = i - r * c.cols;
-    o[i] = norm_code(to_f64(base[r * c.row_stride + col]), lo, den, rden);
-  }
+  for (int64_t r = blockIdx.x; r < c.rows; r += gridDim.x)
+    for (int64_t col = threadIdx.x; col < c.cols; col += blockDim.x)
+      o[r * c.cols + col] = norm_code(to_f64(base[r * c.row_stride + col]), lo, den, rden);
 }
 
 template <typename T>
@@ -174,15 +289,31 @@ int launch_norm(const ut_cube& c, int global, uint8_t* out, double* lohi, int32_
   if (gx < 1) gx = 1;
   norm_init_kernel<<<1, kMaxBands, 0, st>>>(ws);
   UT_CHECK_LAUNCH("norm_init_kernel");
-  norm_minmax_kernel<T><<<dim3((unsigned)gx, c.bands), kThreads, 0, st>>>(c, ws);
+  norm_minmax_kernel<T><<<dim3((unsigned)(c.row_stride == c.cols ? gx : (c.rows < cap ? c.rows : cap)), c.bands),
+                          kThreads, 0, st>>>(c, ws);
   UT_CHECK_LAUNCH("norm_minmax_kernel");
   norm_finish_kernel<<<1, kMaxBands, 0, st>>>(ws, c.bands, global, lohi, flags);
   UT_CHECK_LAUNCH("norm_finish_kernel");
   int64_t gx2 = (n / 16 + kThreads - 1) / kThreads;
   if (gx2 > cap) gx2 = cap;
   if (gx2 < 1) gx2 = 1;
-  norm_codes_kernel<T><<<dim3((unsigned)gx2, c.bands), kThreads, 0, st>>>(c, lohi, out);
-  UT_CHECK_LAUNCH("norm_codes_kernel");
+  if constexpr (sizeof(T) <= 2 && Sample<T>::integral) {
+    constexpr int lut_bytes = 1 << (8 * sizeof(T));
+    if (lut_bytes > 48 * 1024) {
+      static bool attr = false;
+      if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(norm_codes_lut_kernel<T>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, lut_bytes);
+        if (e != cudaSuccess) return cuda_status(e, "norm_codes_lut smem attribute");
+        attr = true;
+      }
+    }
+    norm_codes_lut_kernel<T><<<dim3((unsigned)gx2, c.bands), kThreads, lut_bytes, st>>>(c, lohi, out);
+    UT_CHECK_LAUNCH("norm_codes_lut_kernel");
+  } else {
+    norm_codes_kernel<T><<<dim3((unsigned)gx2, c.bands), kThreads, 0, st>>>(c, lohi, out);
+    UT_CHECK_LAUNCH("norm_codes_kernel");
+  }
   return UT_OK;
 }
 

@@ -80,25 +80,45 @@ sel_hist_kernel(const T* __restrict__ v, int64_t n, int shift, int width, SelWs 
   const typename K::U p0 = (typename K::U)ws.pre[0], p1 = (typename K::U)ws.pre[1];
   const typename K::U mask = ((typename K::U)1 << width) - 1;
   const bool same = p0 == p1;
-  // warp-aggregated shared atomics: score planes concentrate in few bins of
-  // the leading digits, where per-lane atomics would serialize
+  // 4 samples per lane and iteration (one 16/32-byte load); warp-aggregated
+  // shared atomics (score planes concentrate in few bins of the leading digits,
+  // where per-lane atomics would serialize); iterations where no lane matches a
+  // prefix (later passes: almost all) skip the aggregation entirely
   const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
-    const int64_t i = i0 + lane;
-    unsigned b0 = 0xffffffffu, b1 = 0xffffffffu;
-    if (i < n) {
-      const typename K::U k = K::of(v[i]);
-      const typename K::U hi = hs >= K::bits ? 0 : (k >> hs);
-      const unsigned d = (unsigned)((k >> shift) & mask);
-      if (hi == p0) b0 = d;
-      if (!same && hi == p1) b1 = d;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  const bool vec = (reinterpret_cast<uintptr_t>(v) % (4 * sizeof(T))) == 0;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * 4; i0 < n; i0 += stride) {
+    const int64_t i = i0 + 4 * lane;
+    T x[4];
+    if (vec && i + 4 <= n) {
+      if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<uint4*>(x) = ld_stream_u4(v + i);
+      } else {
+        *reinterpret_cast<uint4*>(x) = ld_stream_u4(v + i);
+        *reinterpret_cast<uint4*>(x + 2) = ld_stream_u4(v + i + 2);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) x[j] = i + j < n ? v[i + j] : T(0);
     }
-    const unsigned m0 = __match_any_sync(0xffffffffu, b0);
-    if (b0 != 0xffffffffu && lane == __ffs(m0) - 1) atomicAdd(&h[0][b0], (unsigned)__popc(m0));
-    if (!same) {
-      const unsigned m1 = __match_any_sync(0xffffffffu, b1);
-      if (b1 != 0xffffffffu && lane == __ffs(m1) - 1) atomicAdd(&h[1][b1], (unsigned)__popc(m1));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      unsigned b0 = 0xffffffffu, b1 = 0xffffffffu;
+      if (i + j < n) {
+        const typename K::U k = K::of(x[j]);
+        const typename K::U hi = hs >= K::bits ? 0 : (k >> hs);
+        const unsigned d = (unsigned)((k >> shift) & mask);
+        if (hi == p0) b0 = d;
+        if (!same && hi == p1) b1 = d;
+      }
+      if (__ballot_sync(0xffffffffu, b0 != 0xffffffffu)) {
+        const unsigned m0 = __match_any_sync(0xffffffffu, b0);
+        if (b0 != 0xffffffffu && lane == __ffs(m0) - 1) atomicAdd(&h[0][b0], (unsigned)__popc(m0));
+      }
+      if (!same && __ballot_sync(0xffffffffu, b1 != 0xffffffffu)) {
+        const unsigned m1 = __match_any_sync(0xffffffffu, b1);
+        if (b1 != 0xffffffffu && lane == __ffs(m1) - 1) atomicAdd(&h[1][b1], (unsigned)__popc(m1));
+      }
     }
   }
   __syncthreads();
@@ -108,27 +128,62 @@ sel_hist_kernel(const T* __restrict__ v, int64_t n, int shift, int width, SelWs 
   }
 }
 
-// fix the digit of each rank; clear the histogram for the next pass
-__global__ void sel_scan_kernel(SelWs ws, int width) {
-  __shared__ unsigned int h[2][kBins];
+// fix the digit of each rank; clear the histogram for the next pass.  One
+// block of 1024 threads: per rank, a block-wide inclusive scan of the bins.
+__global__ void __launch_bounds__(1024) sel_scan_kernel(SelWs ws, int width) {
+  __shared__ unsigned long long cum[2][kBins];
+  __shared__ unsigned long long wsum[2][32];
   const bool same = ws.pre[0] == ws.pre[1];
-  for (int i = threadIdx.x; i < 2 * kBins; i += blockDim.x) {
-    (&h[0][0])[i] = ws.hist[i];  // both ranks' histograms
-    ws.hist[i] = 0u;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bins = 1 << width;
+  // each thread owns bins 2 tid, 2 tid + 1 of both histograms
+  unsigned long long a[2][2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int bin = 2 * tid + q;
+      const int src = (same ? 0 : r) * kBins + bin;
+      a[r][q] = bin < bins ? ws.hist[src] : 0ull;
+    }
+  __syncthreads();
+  for (int i = tid; i < 2 * kBins; i += blockDim.x) ws.hist[i] = 0u;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    unsigned long long s = a[r][0] + a[r][1], x = s;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[r][warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned long long w = wsum[r][lane], z = w;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, z, o);
+        if (lane >= o) z += y;
+      }
+      wsum[r][lane] = z - w;  // exclusive warp offsets
+    }
+    __syncthreads();
+    const unsigned long long base = wsum[r][warp] + x - s;  // exclusive before bin 2 tid
+    cum[r][2 * tid] = base + a[r][0];
+    cum[r][2 * tid + 1] = base + a[r][0] + a[r][1];
   }
   __syncthreads();
-  if (threadIdx.x < 2) {
-    const int r = threadIdx.x;
-    const unsigned int* hr = same ? h[0] : h[r];
-    long long rem = ws.rem[r];
-    const int bins = 1 << width;
-    int d = 0;
-    for (; d < bins - 1; ++d) {
-      if (rem <= (long long)hr[d]) break;
-      rem -= hr[d];
+  // the digit: first bin whose inclusive count reaches the rank (ranks read
+  // into registers before any thread rewrites them)
+  const long long rems[2] = {ws.rem[0], ws.rem[1]};
+  __syncthreads();
+  for (int r = 0; r < 2; ++r) {
+    const long long rem = rems[r];
+    for (int bin = tid; bin < bins; bin += blockDim.x) {
+      const unsigned long long before = bin ? cum[r][bin - 1] : 0ull;
+      if ((long long)before < rem && rem <= (long long)cum[r][bin]) {
+        ws.rem[r] = rem - (long long)before;
+        ws.pre[r] = (ws.pre[r] << width) | (unsigned long long)bin;
+      }
     }
-    ws.rem[r] = rem;
-    ws.pre[r] = (ws.pre[r] << width) | (unsigned long long)d;
   }
 }
 
@@ -142,7 +197,7 @@ int launch_select(const T* v, int64_t n, long long r0, long long r1, double* out
                   cudaStream_t st) {
   sel_init_kernel<<<1, 256, 0, st>>>(ws, r0, r1);
   UT_CHECK_LAUNCH("sel_init_kernel");
-  int64_t grid = (n + kThreads - 1) / kThreads;
+  int64_t grid = (n / 4 + kThreads - 1) / kThreads;
   const int64_t cap = (int64_t)sm_count() * 4;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
@@ -152,7 +207,7 @@ int launch_select(const T* v, int64_t n, long long r0, long long r1, double* out
     shift -= width;
     sel_hist_kernel<T><<<(int)grid, kThreads, 0, st>>>(v, n, shift, width, ws);
     UT_CHECK_LAUNCH("sel_hist_kernel");
-    sel_scan_kernel<<<1, 256, 0, st>>>(ws, width);
+    sel_scan_kernel<<<1, 1024, 0, st>>>(ws, width);
     UT_CHECK_LAUNCH("sel_scan_kernel");
   }
   sel_out_kernel<T><<<1, 32, 0, st>>>(ws, out);
