@@ -128,8 +128,16 @@ def dist_setup(n):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # UT_BENCH_BACKEND=gloo (with ranks sharing the GPUs there are) is the
+        # functional check of this multi-rank path on a one-GPU box; timing
+        # runs use NCCL, one GPU per rank
+        backend = os.environ.get("UT_BENCH_BACKEND", "nccl")
+        dev_id = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
+        torch.cuda.set_device(dev_id)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_id))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     return world, rank, local
@@ -440,8 +448,10 @@ def run_b200(args):
     if not args.no_e2e:
         host = host_cube(stack)
         codes_host = torch.empty(pipe.codes.shape, dtype=pipe.codes.dtype, pin_memory=True)
-        h2d = host.numel() * host.element_size() + pipe.xy.numel() * 4 + pipe.cls.numel() * 4 \
-            if cfg.method == "cva" else host.numel() * host.element_size()
+        # the step's inputs: the cube and (CVA) the training set, from pinned host memory
+        train = tuple(t.cpu().pin_memory() for t in (pipe.xy, pipe.cls, pipe.pivots)) \
+            if cfg.method == "cva" else ()
+        h2d = host.numel() * host.element_size() + sum(t.numel() * t.element_size() for t in train)
         d2h = codes_host.numel() * codes_host.element_size()
         times = []
         for i in range(args.e2e_steps + 1):
@@ -450,6 +460,8 @@ def run_b200(args):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             stack.planes.copy_(host, non_blocking=True)
+            if train:
+                pipe.load_training(*train)
             pipe.run()
             codes_host.copy_(pipe.codes, non_blocking=True)
             b.record(stream)
