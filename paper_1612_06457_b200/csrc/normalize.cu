@@ -99,8 +99,25 @@ norm_minmax_kernel(ut_cube c, NormWs ws) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (c.row_stride == c.cols && (reinterpret_cast<uintptr_t>(base) % 16) == 0) {
     constexpr int V = 16 / sizeof(T);
+    constexpr int U = 4;  // 4 independent 16-byte loads in flight per thread
     const int64_t nv = n / V;
-    for (int64_t i = tid; i < nv; i += stride) {
+    const int64_t nu = nv / U * U;
+    for (int64_t i0 = tid; i0 < nu / U; i0 += stride) {
+      T x[U][V];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        *reinterpret_cast<uint4*>(x[u]) = ld_stream_u4(base + V * (i0 + u * (nu / U)));
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          const A a = M::of(x[u][j]);
+          nan |= M::nan(a);
+          mn = M::mn(mn, a);
+          mx = M::mx(mx, a);
+        }
+    }
+    for (int64_t i = nu + tid; i < nv; i += stride) {
       T x[V];
       *reinterpret_cast<uint4*>(x) = ld_stream_u4(base + V * i);
 #pragma unroll
