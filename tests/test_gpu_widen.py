@@ -191,3 +191,42 @@ def test_percentile_on_device_plane_matches_host_codes():
             assert np.array_equal(got, oracle.rescale_percentile(host, p, one_tail=one))
         spec = ut.RenderSpec("percentile", 1.0)
         assert np.array_equal(ut.rescale(dp, spec).cpu().numpy(), oracle.rescale_percentile(host, 1.0))
+
+
+def _select(x, r_lo, r_hi):
+    import ctypes as C
+    from paper_1612_06457_b200 import _lib
+    from paper_1612_06457_b200 import device as dev
+    t = torch.from_numpy(x).cuda()
+    out = torch.empty(2, dtype=torch.float64, device="cuda")
+    L = _lib.lib()
+    ws = dev.workspace("plane_select", L.ut_plane_select_ws(), t.device)
+    ranks = (C.c_int64 * 2)(r_lo, r_hi)
+    dt = _lib.UT_F32 if x.dtype == np.float32 else _lib.UT_F64
+    _lib.check(L.ut_plane_select(t.data_ptr(), dt, x.size, ranks, out.data_ptr(), ws.data_ptr(),
+                                 ws.numel(), dev.stream_handle()), "select")
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_select_sample_blind_spots_fall_back(dtype):
+    """A plane whose strided sample sees only one value: the candidate window
+    misses the ranks and the full radix select (device-gated) must take over."""
+    n = 16384 * 64
+    rng = np.random.default_rng(21)
+    x = rng.normal(size=n).astype(dtype)
+    x[::64] = 0.5                       # exactly the positions the sample reads
+    srt = np.sort(x.astype(np.float64))
+    for r_lo, r_hi in ((1, n), (n // 100, n - n // 100), (n // 2, n // 2 + 1)):
+        lo, hi = _select(x, r_lo, r_hi)
+        assert lo == srt[r_lo - 1] and hi == srt[r_hi - 1]
+
+
+def test_select_heavy_duplicates_and_window_overflow():
+    n = 1 << 23
+    x = np.zeros(n, np.float32)         # > kCandCap equal keys inside one window
+    x[:1000] = np.linspace(-1, 1, 1000, dtype=np.float32)
+    srt = np.sort(x.astype(np.float64))
+    for r_lo, r_hi in ((1, n), (500, n // 2), (n - 10, 3)):
+        lo, hi = _select(x, r_lo, r_hi)
+        assert lo == srt[r_lo - 1] and hi == srt[r_hi - 1]
