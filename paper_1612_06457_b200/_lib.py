@@ -9,12 +9,15 @@ compute entry point raises ``RuntimeError`` (run ``__graft_entry__.build()`` or
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 from .errors import DataError, NumericError
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libundertext_b200.so"
+if os.environ.get("UT_LIB_PATH"):  # dev: a kernel-variant build (tools/build_variant.py)
+    LIB_PATH = Path(os.environ["UT_LIB_PATH"]).resolve()
 
 UT_OK, UT_EDATA, UT_ENUMERIC, UT_ECUDA = 0, 1, 2, 3
 UT_U8, UT_U16, UT_F16, UT_F32, UT_F64 = 0, 1, 2, 3, 4

@@ -163,6 +163,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// The same wait with a suspend-time hint: a warp whose phase is not complete
+// sleeps in the barrier unit (up to `ns`) instead of spinning on try_wait, so
+// waiting warps stop competing for issue slots with the working ones.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(ns)
+      : "memory");
+}
 // One bulk (TMA-engine) copy global -> shared, completing on `bar` (tx bytes).
 // 16-byte aligned addresses and size.  Evict-first L2 policy: streamed once.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,

@@ -511,6 +511,12 @@ constexpr int kImP = 256;                 // pixels per tile
 #define UT_IM_OPP 64
 #define UT_IM_SOP 8
 #endif
+#ifndef UT_IM_SLEEP  // suspend-time hint (ns) of the ring waits; 0 = spin on try_wait
+#define UT_IM_SLEEP 0
+#endif
+#ifndef UT_IM_DSUM   // independent fp64 accumulators of the converters' sample sums
+#define UT_IM_DSUM 1
+#endif
 constexpr int kImStagesIn = UT_IM_SIN;    // input ring: [32][256 + pad] sample rows per stage
 constexpr int kImOpP = UT_IM_OPP;         // pixels per operand buffer (MMAs of K = 32)
 constexpr int kImStagesOp = UT_IM_SOP;    // operand ring
@@ -547,6 +553,11 @@ struct ImParams {
   int dbg;            // dev probes: 1 = no MMA, 2 = no conversion
   long long* part;    // [G]: int64 [4][32][33] digit-row records, then fp64 [32] sums of x - s
 };
+
+__device__ __forceinline__ void im_wait(uint64_t* bar, uint32_t parity) {
+  if (UT_IM_SLEEP > 0) mbar_wait_sleep(bar, parity, UT_IM_SLEEP);
+  else mbar_wait(bar, parity);
+}
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   // K-major, no swizzle: 8-row x 16-byte core matrices; rows of a core matrix
@@ -681,7 +692,7 @@ region_imma_kernel(ImParams r) {
       const int nb = B > warp ? (B - 1 - warp) / kImProd + 1 : 0;
       for (int i = 0; i < nloc; ++i) {
         const int st = i % kImStagesIn;
-        if (i >= kImStagesIn) mbar_wait(&in_empty[st], ((i / kImStagesIn) - 1) & 1);
+        if (i >= kImStagesIn) im_wait(&in_empty[st], ((i / kImStagesIn) - 1) & 1);
         const int64_t p0 = ((int64_t)blockIdx.x + (int64_t)i * r.G) * kImP;
         const int64_t npx = (r.npix - p0) < kImP ? (r.npix - p0) : kImP;
         const uint32_t bytes = (uint32_t)(npx * sizeof(T));
@@ -698,7 +709,7 @@ region_imma_kernel(ImParams r) {
       const uint32_t op0 = smem_u32(op);
       for (int u = 0; u < H * nloc; ++u) {
         const int o = u % kImStagesOp;
-        mbar_wait(&op_full[o], (u / kImStagesOp) & 1);
+        im_wait(&op_full[o], (u / kImStagesOp) & 1);
         const int w = u / (H * kImWindowTiles), a = w & 1;
         const bool first = (u % (H * kImWindowTiles)) == 0;
         const bool last = (u % (H * kImWindowTiles)) == H * kImWindowTiles - 1 || u == H * nloc - 1;
@@ -727,7 +738,9 @@ region_imma_kernel(ImParams r) {
     const int b = lane;
     const double scale = b < B ? r.scale[b] : 0.0;
     const double addend = b < B ? r.addend[b] : 0.0;
-    double dsum = 0.0;  // fp64 sum of the samples: the mean does not see the grid
+    double dsum[UT_IM_DSUM];  // fp64 sums of the samples: the mean does not see the grid
+#pragma unroll
+    for (int q = 0; q < UT_IM_DSUM; ++q) dsum[q] = 0.0;
     uint32_t bad = 0;
     // epilogue thread: digit row 32 i + b, 32 Gram columns + the ones column
     long long* rec = r.part + (size_t)blockIdx.x * kImRec +
@@ -768,8 +781,8 @@ region_imma_kernel(ImParams r) {
     for (int i = 0; i < nloc; ++i) {
       const int u = H * i + cw / CPB;
       const int st = i % kImStagesIn, o = u % kImStagesOp;
-      mbar_wait(&in_full[st], (i / kImStagesIn) & 1);
-      if (u >= kImStagesOp) mbar_wait(&op_empty[o], ((u / kImStagesOp) - 1) & 1);
+      im_wait(&in_full[st], (i / kImStagesIn) & 1);
+      if (u >= kImStagesOp) im_wait(&op_empty[o], ((u / kImStagesOp) - 1) & 1);
       const int64_t p0 = ((int64_t)blockIdx.x + (int64_t)i * r.G) * kImP;
       const int npx = (int)((r.npix - p0) < kImP ? (r.npix - p0) : kImP);
       const T* stage = in + (size_t)st * kMaxBands * PS;
@@ -795,7 +808,7 @@ region_imma_kernel(ImParams r) {
               const double t = fma(xw, scale, addend);
               bad |= (uint32_t)__double2hiint(t) ^ 0x43380000u;
               wd[p] = (uint32_t)__double2loint(t);
-              dsum += xw;
+              dsum[p % UT_IM_DSUM] += xw;
             }
           } else {
 #pragma unroll
@@ -805,7 +818,7 @@ region_imma_kernel(ImParams r) {
               const bool ok = p < valid;
               bad |= ok ? ((uint32_t)__double2hiint(t) ^ 0x43380000u) : 0u;
               wd[p] = ok ? (uint32_t)__double2loint(t) : 0x80808080u;  // v = 0 past the end
-              dsum += ok ? xw : 0.0;
+              dsum[p % UT_IM_DSUM] += ok ? xw : 0.0;
             }
           }
           uint32_t o0[4], o1[4], o2[4], o3[4];
@@ -827,7 +840,10 @@ region_imma_kernel(ImParams r) {
     }
     if (epi && nloc > 0) flush((nloc - 1) / kImWindowTiles);
     if (bad) atomicOr(&bad_any, 1);
-    xsum[cw][b] = dsum;
+    double ds = dsum[0];
+#pragma unroll
+    for (int q = 1; q < UT_IM_DSUM; ++q) ds += dsum[q];
+    xsum[cw][b] = ds;
   }
   tc_fence_before();
   __syncthreads();
