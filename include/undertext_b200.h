@@ -228,6 +228,29 @@ int ut_synth_cube(const ut_cube* cube, int64_t height, const double* means,
 int ut_class_of(const int64_t* shapes, int32_t nshapes, const int32_t* xy,
                 int64_t n, int32_t* cls, void* stream);
 
+/* ------------------------------------------------- image encoders
+ * save_image (rendering.py:303-331) replaces cv2.imwrite (libpng / libtiff).
+ * img: device, (rows, cols, channels) C-contiguous uint8 (depth 8) or uint16
+ * (depth 16), channels 1 (gray) or 3 (RGB).  format 0 = PNG, 1 = TIFF.
+ * ut_encode_png writes the PNG's IDAT chunks (zlib stream of the row-filtered
+ * image, chunk CRCs included) to `out`; the caller frames them with the
+ * signature, IHDR and IEND.  ut_encode_tiff writes the strips back to back
+ * (compression 1 = raw, 8 = one zlib stream per strip over Predictor-2
+ * samples) with strip_bytes[s] (device, ceil(rows / rows_per_strip) entries);
+ * the caller adds the header and IFD.  *out_len (device) = bytes written.
+ * Output bytes depend only on the image (deterministic). */
+size_t ut_encode_ws(int64_t rows, int64_t cols, int32_t channels, int32_t depth, int32_t format,
+                    int64_t rows_per_strip);
+int64_t ut_encode_bound(int64_t rows, int64_t cols, int32_t channels, int32_t depth,
+                        int32_t format, int64_t rows_per_strip);
+int ut_encode_png(const void* img, int64_t rows, int64_t cols, int32_t channels, int32_t depth,
+                  uint8_t* out, int64_t out_cap, int64_t* out_len, void* ws, size_t ws_bytes,
+                  void* stream);
+int ut_encode_tiff(const void* img, int64_t rows, int64_t cols, int32_t channels, int32_t depth,
+                   int32_t compression, int64_t rows_per_strip, uint8_t* out, int64_t out_cap,
+                   int64_t* strip_bytes, int64_t* out_len, void* ws, size_t ws_bytes,
+                   void* stream);
+
 #ifdef __cplusplus
 }
 #endif

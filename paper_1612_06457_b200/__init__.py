@@ -12,6 +12,7 @@ from .annotations import (AnnotatedPoint, ClassLabel, DesignMatrix, TrainingSet,
                           assemble_matrix)
 from .eigen import (DEFAULT_RIDGE, EigenSolution, regularize, sign_normalize,  # noqa: F401
                     solve_gen_eig_sym)
+from .image_io import encode_png, encode_tiff, save_image  # noqa: F401
 from .errors import DataError, NumericError, UndertextError, UndertextWarning  # noqa: F401
 from .pipeline import CvaPipeline, FolioStream, PcaPipeline, route_points, row_bounds  # noqa: F401
 from .projection import (ALL_METHODS, METHOD_CVA, METHOD_LDA, METHOD_PCA,  # noqa: F401
