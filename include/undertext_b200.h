@@ -228,6 +228,13 @@ int ut_synth_cube(const ut_cube* cube, int64_t height, const double* means,
 int ut_class_of(const int64_t* shapes, int32_t nshapes, const int32_t* xy,
                 int64_t n, int32_t* cls, void* stream);
 
+/* ------------------------------------------------- composites
+ * compose_rgb (rendering.py:206-225): out[3 i + c] = plane_c[i] for three
+ * device code planes of npix samples (depth 8: uint8, 16: uint16), the
+ * recipe's channel choice and swap already applied by the caller. */
+int ut_compose_rgb(const void* r, const void* g, const void* b, int32_t depth, int64_t npix,
+                   void* out, void* stream);
+
 /* ------------------------------------------------- image encoders
  * save_image (rendering.py:303-331) replaces cv2.imwrite (libpng / libtiff).
  * img: device, (rows, cols, channels) C-contiguous uint8 (depth 8) or uint16

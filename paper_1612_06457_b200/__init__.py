@@ -14,13 +14,16 @@ from .eigen import (DEFAULT_RIDGE, EigenSolution, regularize, sign_normalize,  #
                     solve_gen_eig_sym)
 from .image_io import encode_png, encode_tiff, save_image  # noqa: F401
 from .errors import DataError, NumericError, UndertextError, UndertextWarning  # noqa: F401
-from .pipeline import CvaPipeline, FolioStream, PcaPipeline, route_points, row_bounds  # noqa: F401
+from .pipeline import (CvaPipeline, FolioStream, PcaPipeline, RenderResult,  # noqa: F401
+                       composite_filename, plane_filename, render_planes, route_points,
+                       row_bounds)
 from .projection import (ALL_METHODS, METHOD_CVA, METHOD_LDA, METHOD_PCA,  # noqa: F401
                          METHOD_PCA_UNSUPERVISED, ProjectionModel, ScatterPair,
                          compute_scatter, fit, fit_cva, fit_pca, fit_pca_unsupervised,
                          project_stack)
 from .quantize import code_dtype, linear_to_codes, max_code, round_half_away  # noqa: F401
-from .rendering import (PERCENTILE_CHOICES, DeviceScorePlane, RenderSpec,  # noqa: F401
+from .rendering import (PERCENTILE_CHOICES, CompositeRecipe, DeviceScorePlane,  # noqa: F401
+                        RenderSpec, compose_rgb,
                         ScorePlane, nearest_rank_percentile, rescale, rescale_full,
                         rescale_percentile, rescale_training_range)
 from .stack import BandMeta, DeviceStack, SpectralStack, normalize_stack  # noqa: F401

@@ -31,7 +31,7 @@ EXPORTS = (
     "ut_stretch", "ut_plane_minmax_ws", "ut_plane_minmax", "ut_linear_to_codes",
     "ut_plane_select_ws", "ut_plane_select", "ut_normalize_ws", "ut_normalize_stack",
     "ut_synth_cube", "ut_class_of", "ut_encode_ws", "ut_encode_bound", "ut_encode_png",
-    "ut_encode_tiff",
+    "ut_encode_tiff", "ut_compose_rgb",
 )
 
 
@@ -81,6 +81,7 @@ _SIGS = {
     "ut_normalize_stack": (I32, [C.POINTER(Cube), I32, P, P, P, P, SZ, P]),
     "ut_synth_cube": (I32, [C.POINTER(Cube), I64, P, P, I32, P, I32, C.c_uint64, P]),
     "ut_class_of": (I32, [P, I32, P, I64, P, P]),
+    "ut_compose_rgb": (I32, [P, P, P, I32, I64, P, P]),
     "ut_encode_ws": (SZ, [I64, I64, I32, I32, I32, I64]),
     "ut_encode_bound": (I64, [I64, I64, I32, I32, I32, I64]),
     "ut_encode_png": (I32, [P, I64, I64, I32, I32, P, I64, P, P, SZ, P]),

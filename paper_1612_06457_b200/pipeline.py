@@ -18,6 +18,9 @@ size) and the 2K min/max record (all_reduce MAX).  Errors found on the device
 
 from __future__ import annotations
 
+from dataclasses import dataclass, field
+from pathlib import Path
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -29,8 +32,9 @@ from .eigen import DEFAULT_RIDGE, raise_for_info
 from .errors import DataError
 from .projection import (CvaDevice, PcaDevice, ProjectionModel, METHOD_CVA,
                          METHOD_PCA_UNSUPERVISED, class_index, project_device, _top_k)
-from .rendering import stretch_planes
-from .stack import DeviceStack
+from .rendering import (CompositeRecipe, RenderSpec, _zeros_warning, compose_rgb, rescale,
+                        stretch_planes)
+from .stack import DeviceStack, on_device
 
 
 def row_bounds(height: int, world: int, rank: int) -> tuple[int, int]:
@@ -342,3 +346,81 @@ class FolioStream:
     def check(self):
         for p in self.pipes:
             p.check()
+
+
+# ------------------------------------------------------------ render_planes
+# Components projected per K4 pass (the kernel's limit); the reference batches
+# 8 planes at a time to bound host memory (pipeline.py:44), re-reading the
+# cube once per batch.
+_RENDER_BATCH = 32
+
+
+@dataclass
+class RenderResult:
+    """Artifact paths written by render_planes, in deterministic order
+    (pipeline.py:120-125)."""
+
+    plane_paths: list[Path] = field(default_factory=list)
+    composite_path: Path | None = None
+
+
+def plane_filename(run_name: str, k: int, spec: RenderSpec, fmt: str) -> str:
+    return f"{run_name}_plane{k:02d}{spec.suffix()}.{fmt}"
+
+
+def composite_filename(run_name: str, recipe: CompositeRecipe) -> str:
+    return f"{run_name}{recipe.suffix()}.png"
+
+
+def render_planes(stack, model: ProjectionModel, specs: list[RenderSpec], out_dir,
+                  run_name: str = "run", components: list[int] | None = None,
+                  recipe: CompositeRecipe | None = None, workers: int = 1, fmt: str = "png",
+                  compression: str = "none") -> RenderResult:
+    """Project, rescale per spec, and write one grayscale image per plane per
+    spec, plus the optional composite (pipeline.py:136-190), entirely on the
+    device: one K4 pass projects every requested component (score planes stay
+    in HBM), each spec renders codes on the device (full range from the
+    projector's min/max, training range, percentile select), compose_rgb
+    interleaves the recipe's planes, and the PNG / TIFF bytes are encoded on
+    the device; the host writes finished files.  Same files, names and order
+    as the reference; ``workers`` is accepted for signature compatibility."""
+    from .image_io import save_image
+    from .projection import project_stack
+
+    if fmt not in ("png", "tif"):
+        raise DataError(f"format must be png or tif, got {fmt!r}")
+    if not specs:
+        raise DataError("at least one render spec required")
+    out_dir = Path(out_dir)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    if components is None:
+        components = list(range(model.component_count))
+    ds = on_device(stack)
+    result = RenderResult()
+    needed = set() if recipe is None else {recipe.red, recipe.green, recipe.blue}
+    recipe_planes: dict = {}
+    for i in range(0, len(components), _RENDER_BATCH):
+        batch = components[i:i + _RENDER_BATCH]
+        planes = project_stack(ds, model, components=batch, workers=workers)
+        ranges = planes[0].minmax.cpu().numpy()   # [-min_0.., max_0..] of the batch
+        nb = len(batch)
+        for j, (k, plane) in enumerate(zip(batch, planes)):
+            for s_i, spec in enumerate(specs):
+                if spec.mode == "full" and -ranges[j] == ranges[nb + j]:
+                    _zeros_warning("constant score plane")   # rendering.py:128-129
+                img = rescale(plane, spec, model=model, k=k)
+                path = out_dir / plane_filename(run_name, k, spec, fmt)
+                save_image(img, path, compression=compression)
+                result.plane_paths.append(path)
+                if s_i == 0 and k in needed:
+                    recipe_planes[k] = img
+    if recipe is not None:
+        missing = sorted(needed - set(recipe_planes))
+        if missing:
+            raise DataError(f"recipe needs planes {missing}, not rendered")
+        trio = [recipe_planes[recipe.red], recipe_planes[recipe.green], recipe_planes[recipe.blue]]
+        composite = compose_rgb(trio, CompositeRecipe(0, 1, 2, swap=recipe.swap))
+        path = out_dir / composite_filename(run_name, recipe)
+        save_image(composite, path)
+        result.composite_path = path
+    return result

@@ -8,7 +8,9 @@ plane of the projector's output, with the min/max the projector already
 reduced) is rescaled by ``ut_stretch`` without another reduction pass.
 The training-range and percentile modes (:133-179) use the same
 ``ut_linear_to_codes``; the percentile window comes from an exact radix select
-on the device (``ut_plane_select``).  Composites and codecs are outside the path.
+on the device (``ut_plane_select``).  ``compose_rgb`` (:206-225) interleaves
+three code planes on the device (``ut_compose_rgb``); files are written by
+``image_io.save_image`` (device PNG / TIFF encoders).
 """
 
 from __future__ import annotations
@@ -265,3 +267,70 @@ def rescale(plane, spec: RenderSpec, model=None, k: int | None = None):
             raise DataError("training-range rescale needs the fitted model and plane index")
         return rescale_training_range(plane, model, k, spec.out_depth)
     return rescale_percentile(plane, spec.percentile_p, spec.out_depth, spec.one_tail)
+
+
+# ---------------------------------------------------------------- composites
+
+@dataclass(frozen=True)
+class CompositeRecipe:
+    """Which rendered planes land in R, G, B, with an optional channel swap
+    (a pair of channel indices, 0=R 1=G 2=B, exchanged after assignment)
+    (rendering.py:96-116)."""
+
+    red: int
+    green: int
+    blue: int
+    swap: tuple[int, int] | None = None
+
+    def __post_init__(self):
+        if self.swap is not None:
+            a, b = self.swap
+            if not {a, b} <= {0, 1, 2} or a == b:
+                raise DataError(f"swap must name two distinct channels, got {self.swap}")
+
+    def suffix(self) -> str:
+        text = f"_R{self.red}G{self.green}B{self.blue}"
+        if self.swap is not None:
+            text += f"_swap{self.swap[0]}{self.swap[1]}"
+        return text
+
+
+def _code_depth(img, name: str = "image") -> int:
+    dt = img.dtype
+    if dt in (np.uint8, torch.uint8):
+        return 8
+    if dt in (np.uint16, torch.uint16):
+        return 16
+    raise DataError(f"{name} must be uint8 or uint16, got {dt}")
+
+
+def compose_rgb(planes: list, recipe: CompositeRecipe):
+    """Stack three rendered planes into an RGB image per the recipe
+    (rendering.py:206-225).  Recipe indices select from ``planes`` (repeats
+    allowed); the optional swap exchanges two finished channels afterwards.
+    Device planes -> device (H, W, 3) tensor; host arrays -> numpy."""
+    for idx in (recipe.red, recipe.green, recipe.blue):
+        if not (0 <= idx < len(planes)):
+            raise DataError(f"recipe index {idx} outside plane set of {len(planes)}")
+    channels = [planes[recipe.red], planes[recipe.green], planes[recipe.blue]]
+    depths = {_code_depth(c) for c in channels}
+    shapes = {tuple(c.shape) for c in channels}
+    if len(shapes) != 1 or len(depths) != 1:
+        raise DataError("composite channels must share dimensions and bit depth")
+    if any(len(c.shape) != 2 for c in channels):
+        raise DataError("composite channels must be grayscale")
+    if recipe.swap is not None:
+        a, b = recipe.swap
+        channels[a], channels[b] = channels[b], channels[a]
+    host = not isinstance(channels[0], torch.Tensor)
+    device = dev.require_cuda() if host else channels[0].device
+    chans = [dev.to_device(c, device) if (host or not c.is_cuda or not c.is_contiguous())
+             else c for c in channels]
+    h, w = chans[0].shape
+    depth = depths.pop()
+    out = torch.empty((h, w, 3), dtype=_torch_code_dtype(depth), device=device)
+    with torch.cuda.device(device):
+        _lib.check(_lib.lib().ut_compose_rgb(chans[0].data_ptr(), chans[1].data_ptr(),
+                                             chans[2].data_ptr(), depth, h * w, out.data_ptr(),
+                                             dev.stream_handle()), "ut_compose_rgb")
+    return out.cpu().numpy() if host else out

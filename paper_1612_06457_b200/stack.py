@@ -131,7 +131,9 @@ class DeviceStack:
     @classmethod
     def from_host(cls, stack: SpectralStack, device=None) -> "DeviceStack":
         device = device or dev.require_cuda()
-        t = torch.from_numpy(np.ascontiguousarray(stack.planes))
+        with warnings.catch_warnings():  # read-only planes: only ever copied to the device
+            warnings.simplefilter("ignore", UserWarning)
+            t = torch.from_numpy(np.ascontiguousarray(stack.planes))
         return cls(stack.bands, t.to(device), stack.bit_depth, stack.normalized)
 
 

@@ -72,3 +72,20 @@ def test_check_image_messages():
     with pytest.raises(DataError, match="2-D or 3-D"):
         image_io.check_image(np.zeros((2,), dtype=np.uint8))
     assert image_io.check_image(np.zeros((2, 2, 3), dtype=np.uint16)) == (16, 3)
+
+
+def test_render_names_and_recipe_validation(tmp_path):
+    import paper_1612_06457_b200 as ut
+    assert ut.CompositeRecipe(0, 1, 2).suffix() == "_R0G1B2"
+    assert ut.CompositeRecipe(0, 1, 2, swap=(1, 2)).suffix() == "_R0G1B2_swap12"
+    with pytest.raises(DataError):
+        ut.CompositeRecipe(0, 1, 2, swap=(1, 1))
+    with pytest.raises(DataError):
+        ut.CompositeRecipe(0, 1, 2, swap=(0, 3))
+    spec = ut.RenderSpec("percentile", 0.1)
+    assert ut.plane_filename("run", 3, spec, "png") == "run_plane03_p0_1.png"
+    assert ut.composite_filename("run", ut.CompositeRecipe(2, 1, 0)) == "run_R2G1B0.png"
+    with pytest.raises(DataError, match="format"):
+        ut.render_planes(None, None, [spec], tmp_path, fmt="jpg")
+    with pytest.raises(DataError, match="spec"):
+        ut.render_planes(None, None, [], tmp_path)
