@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import threading
+import warnings
 import weakref
 from dataclasses import dataclass, field
 
