@@ -267,6 +267,13 @@ struct Codes {
   uint32_t header_bits;
 };
 
+// histogram add aggregated over the lanes of the warp that are here with the
+// same symbol (the parse loops diverge; hot symbols would serialize otherwise)
+__device__ __forceinline__ void hist_add(uint32_t* h, int sym) {
+  const unsigned mask = __match_any_sync(__activemask(), sym);
+  if ((threadIdx.x & 31) == __ffs(mask) - 1) atomicAdd(&h[sym], (uint32_t)__popc(mask));
+}
+
 __device__ __forceinline__ int fixed_litlen_len(int s) {
   return s < 144 ? 8 : (s < 256 ? 9 : (s < 280 ? 7 : 8));
 }
@@ -277,8 +284,8 @@ __device__ __forceinline__ int fixed_litlen_len(int s) {
 //   MODE 1: return the bits under cd's code tables;
 //   MODE 2: write the codes at `pos` with cd's tables.
 template <int MODE>
-__device__ uint32_t parse_range(const uint8_t* buf, int base, int q0, int q1, const DeflateParams& p,
-                                Codes* cd, uint32_t* words, uint32_t pos) {
+__device__ uint32_t parse_range(const uint8_t* buf, int base, int q0, int q1, const int* cand,
+                                int ncand, Codes* cd, uint32_t* words, uint32_t pos) {
   uint32_t nbits = 0;
   int q = q0;
   while (q < q1) {
@@ -287,12 +294,13 @@ __device__ uint32_t parse_range(const uint8_t* buf, int base, int q0, int q1, co
     int bl = 0, bd = 0;
     if (maxl >= 3) {
       const uint8_t x0 = buf[at], x1 = buf[at + 1], x2 = buf[at + 2];
-      for (int c = 0; c < p.ncand; ++c) {
-        const int d = p.cand[c];
+      for (int c = 0; c < ncand; ++c) {
+        const int d = cand[c];
         if (d > at) break;
         const uint8_t* a = buf + at;
         const uint8_t* b = a - d;
-        if (b[0] != x0 || b[1] != x1 || b[2] != x2) continue;
+        if (b[0] != x0) continue;           // most candidates fail on the first byte
+        if (b[1] != x1 || b[2] != x2) continue;
         int l = 3;
         while (l < maxl && a[l] == b[l]) ++l;
         if (l > bl) {
@@ -307,8 +315,8 @@ __device__ uint32_t parse_range(const uint8_t* buf, int base, int q0, int q1, co
       length_sym(bl, &sym, &nx, &xv);
       dist_sym(bd, &dsy, &dnx, &dxv);
       if (MODE == 0) {
-        atomicAdd(&cd->lf[sym], 1u);
-        atomicAdd(&cd->df[dsy], 1u);
+        hist_add(cd->lf, sym);
+        hist_add(cd->df, dsy);
         nbits += fixed_litlen_len(sym) + nx + 5 + dnx;
       } else {
         const int n1 = cd->llen[sym], n2 = cd->dlen[dsy];
@@ -322,7 +330,7 @@ __device__ uint32_t parse_range(const uint8_t* buf, int base, int q0, int q1, co
     } else {
       const int lit = buf[at];
       if (MODE == 0) {
-        atomicAdd(&cd->lf[lit], 1u);
+        hist_add(cd->lf, lit);
         nbits += fixed_litlen_len(lit);
       } else {
         nbits += cd->llen[lit];
@@ -412,9 +420,9 @@ __device__ void canon_codes(const uint8_t* len, int n, uint16_t* code) {
     code[i] = len[i] ? (uint16_t)rev_bits((uint32_t)next[len[i]]++, len[i]) : 0;
 }
 
-// Dynamic-Huffman tables of the unit from cd->lf / cd->df and its block header
-// (BFINAL = 0, BTYPE = 10) written at bit 0; sets cd->header_bits.
-__device__ void build_dynamic(Codes* cd, uint32_t* words, bool write) {
+// Dynamic-Huffman tables of the unit from cd->lf / cd->df, the run-length coded
+// code lengths and the size of the block header (cd->header_bits).
+__device__ void build_dynamic(Codes* cd) {
   if (threadIdx.x == 0) cd->lf[256] = 1;  // end of block
   __syncthreads();
   huff_lengths(cd->lf, 286, 15, cd->llen, cd);
@@ -477,21 +485,24 @@ __device__ void build_dynamic(Codes* cd, uint32_t* words, bool write) {
       bits += cd->clen[sym] + (sym == 16 ? 2 : sym == 17 ? 3 : sym == 18 ? 7 : 0);
     }
     cd->header_bits = bits;
-    if (write) {
-      uint32_t pos = 0;
-      put_bits(words, pos, 4u, 3);  // BFINAL = 0, BTYPE = 10
-      put_bits(words, pos, (uint32_t)(cd->hlit - 257), 5);
-      put_bits(words, pos, (uint32_t)(cd->hdist - 1), 5);
-      put_bits(words, pos, (uint32_t)(hclen - 4), 4);
-      for (int i = 0; i < hclen; ++i) put_bits(words, pos, cd->clen[order[i]], 3);
-      for (int i = 0; i < cd->nrle; ++i) {
-        const int sym = cd->rle[i] & 31, ex = cd->rle[i] >> 5;
-        const int nx = sym == 16 ? 2 : sym == 17 ? 3 : sym == 18 ? 7 : 0;
-        put_bits(words, pos, cd->ccode[sym] | ((uint32_t)ex << cd->clen[sym]), cd->clen[sym] + nx);
-      }
-    }
   }
   __syncthreads();
+}
+
+// block header (BFINAL = 0, BTYPE = 10) at bit 0, one thread
+__device__ void write_dynamic_header(const Codes* cd, uint32_t* words) {
+  const uint8_t order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+  uint32_t pos = 0;
+  put_bits(words, pos, 4u, 3);
+  put_bits(words, pos, (uint32_t)(cd->hlit - 257), 5);
+  put_bits(words, pos, (uint32_t)(cd->hdist - 1), 5);
+  put_bits(words, pos, (uint32_t)(cd->hclen - 4), 4);
+  for (int i = 0; i < cd->hclen; ++i) put_bits(words, pos, cd->clen[order[i]], 3);
+  for (int i = 0; i < cd->nrle; ++i) {
+    const int sym = cd->rle[i] & 31, ex = cd->rle[i] >> 5;
+    const int nx = sym == 16 ? 2 : sym == 17 ? 3 : sym == 18 ? 7 : 0;
+    put_bits(words, pos, cd->ccode[sym] | ((uint32_t)ex << cd->clen[sym]), cd->clen[sym] + nx);
+  }
 }
 
 __device__ void fixed_tables(Codes* cd) {
@@ -554,6 +565,9 @@ __global__ void __launch_bounds__(kDThreads) deflate_kernel(DeflateParams p) {
   for (int i = threadIdx.x; i < kWords; i += blockDim.x) words[i] = 0u;
   for (int i = threadIdx.x; i < 288; i += blockDim.x) cd->lf[i] = 0u;
   for (int i = threadIdx.x; i < 32; i += blockDim.x) cd->df[i] = 0u;
+  __shared__ int cand[kMaxCand];
+  if (threadIdx.x < kMaxCand) cand[threadIdx.x] = p.cand[threadIdx.x];
+  const int ncand = p.ncand;
   __syncthreads();
 
   const int q0 = min(g.len, (int)threadIdx.x * kSub), q1 = min(g.len, q0 + kSub);
@@ -564,7 +578,7 @@ __global__ void __launch_bounds__(kDThreads) deflate_kernel(DeflateParams p) {
     sa += b;
     sb += (uint64_t)(g.len - q) * b;
   }
-  const uint32_t nb_fixed = parse_range<0>(buf, g.hist, q0, q1, p, cd, nullptr, 0);
+  const uint32_t nb_fixed = parse_range<0>(buf, g.hist, q0, q1, cand, ncand, cd, nullptr, 0);
   uint64_t fixed_bits;
   block_exclusive_scan(nb_fixed, &fixed_bits);
   {
@@ -576,8 +590,8 @@ __global__ void __launch_bounds__(kDThreads) deflate_kernel(DeflateParams p) {
       p.uadler[2 * u + 1] = (uint32_t)(t_sb % kAdlerMod);
     }
   }
-  build_dynamic(cd, words, false);
-  const uint32_t nb_dyn = parse_range<1>(buf, g.hist, q0, q1, p, cd, nullptr, 0);
+  build_dynamic(cd);
+  const uint32_t nb_dyn = parse_range<1>(buf, g.hist, q0, q1, cand, ncand, cd, nullptr, 0);
   uint64_t dyn_bits;
   const uint64_t dyn_before = block_exclusive_scan(nb_dyn, &dyn_bits);
   // block + end of block + empty stored block header (sync flush), padded,
@@ -591,19 +605,19 @@ __global__ void __launch_bounds__(kDThreads) deflate_kernel(DeflateParams p) {
   if (coded <= g.len + 5) {
     uint32_t pos;
     if (use_dyn) {
-      build_dynamic(cd, words, true);   // same tables, now with the header written
+      if (threadIdx.x == 0) write_dynamic_header(cd, words);
       pos = cd->header_bits + (uint32_t)dyn_before;
     } else {
       // fixed path: recount positions under the fixed tables
       __syncthreads();
       fixed_tables(cd);
-      const uint32_t nb = parse_range<1>(buf, g.hist, q0, q1, p, cd, nullptr, 0);
+      const uint32_t nb = parse_range<1>(buf, g.hist, q0, q1, cand, ncand, cd, nullptr, 0);
       uint64_t tot;
       pos = 3 + (uint32_t)block_exclusive_scan(nb, &tot);
       if (threadIdx.x == 0) words[0] |= 2u;  // BFINAL = 0, BTYPE = 01
     }
     __syncthreads();
-    parse_range<2>(buf, g.hist, q0, q1, p, cd, words, pos);
+    parse_range<2>(buf, g.hist, q0, q1, cand, ncand, cd, words, pos);
     __syncthreads();
     if (threadIdx.x == 0) {  // end of block (zero bits for the fixed code)
       uint32_t e = (use_dyn ? cd->header_bits + (uint32_t)dyn_bits : 3 + (uint32_t)fixed_bits);
