@@ -258,6 +258,21 @@ int ut_encode_tiff(const void* img, int64_t rows, int64_t cols, int32_t channels
                    int64_t* strip_bytes, int64_t* out_len, void* ws, size_t ws_bytes,
                    void* stream);
 
+/* ------------------------------------------------- image decode
+ * load_stack / load_image (stack.py:119-177, rendering.py:334-343) replace
+ * cv2.imread for TIFF bands.  src: the file's bytes in device memory; strip i
+ * is in_len[i] bytes at in_off[i] and decodes to out_len[i] bytes at
+ * dst + out_off[i] (all four arrays device).  compression 1 = raw strips,
+ * 8 = one zlib stream per strip (Adler-32 checked).  status[i] (device) = 0,
+ * or nonzero if strip i is malformed / too short / too long.
+ * ut_unpredict undoes TIFF Predictor 2 (horizontal differencing per channel)
+ * in place, after swapping the bytes of big-endian 16-bit samples if asked. */
+int ut_decode_strips(const uint8_t* src, const int64_t* in_off, const int64_t* in_len, int64_t nstrips,
+                     int32_t compression, uint8_t* dst, const int64_t* out_off, const int64_t* out_len,
+                     int32_t* status, void* stream);
+int ut_unpredict(void* img, int32_t depth, int64_t rows, int64_t cols, int32_t channels,
+                 int32_t predictor, int32_t swap_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

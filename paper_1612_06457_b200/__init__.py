@@ -12,7 +12,7 @@ from .annotations import (AnnotatedPoint, ClassLabel, DesignMatrix, TrainingSet,
                           assemble_matrix)
 from .eigen import (DEFAULT_RIDGE, EigenSolution, regularize, sign_normalize,  # noqa: F401
                     solve_gen_eig_sym)
-from .image_io import encode_png, encode_tiff, save_image  # noqa: F401
+from .image_io import encode_png, encode_tiff, load_image, save_image  # noqa: F401
 from .errors import DataError, NumericError, UndertextError, UndertextWarning  # noqa: F401
 from .pipeline import (CvaPipeline, FolioStream, PcaPipeline, RenderResult,  # noqa: F401
                        composite_filename, plane_filename, render_planes, route_points,
@@ -26,6 +26,7 @@ from .rendering import (PERCENTILE_CHOICES, CompositeRecipe, DeviceScorePlane,  
                         RenderSpec, compose_rgb,
                         ScorePlane, nearest_rank_percentile, rescale, rescale_full,
                         rescale_percentile, rescale_training_range)
-from .stack import BandMeta, DeviceStack, SpectralStack, normalize_stack  # noqa: F401
+from .stack import (BandMeta, DeviceStack, SpectralStack, crop, load_device_stack,  # noqa: F401
+                    load_stack, normalize_stack)
 
 __version__ = "0.1.0"

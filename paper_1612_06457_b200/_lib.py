@@ -31,7 +31,7 @@ EXPORTS = (
     "ut_stretch", "ut_plane_minmax_ws", "ut_plane_minmax", "ut_linear_to_codes",
     "ut_plane_select_ws", "ut_plane_select", "ut_normalize_ws", "ut_normalize_stack",
     "ut_synth_cube", "ut_class_of", "ut_encode_ws", "ut_encode_bound", "ut_encode_png",
-    "ut_encode_tiff", "ut_compose_rgb",
+    "ut_encode_tiff", "ut_compose_rgb", "ut_decode_strips", "ut_unpredict",
 )
 
 
@@ -82,6 +82,8 @@ _SIGS = {
     "ut_synth_cube": (I32, [C.POINTER(Cube), I64, P, P, I32, P, I32, C.c_uint64, P]),
     "ut_class_of": (I32, [P, I32, P, I64, P, P]),
     "ut_compose_rgb": (I32, [P, P, P, I32, I64, P, P]),
+    "ut_decode_strips": (I32, [P, P, P, I64, I32, P, P, P, P, P]),
+    "ut_unpredict": (I32, [P, I32, I64, I64, I32, I32, I32, P]),
     "ut_encode_ws": (SZ, [I64, I64, I32, I32, I32, I64]),
     "ut_encode_bound": (I64, [I64, I64, I32, I32, I32, I64]),
     "ut_encode_png": (I32, [P, I64, I64, I32, I32, P, I64, P, P, SZ, P]),

@@ -1,0 +1,309 @@
+// Band-image decode for load_stack / load_image (stack.py:119-177,
+// rendering.py:334-343): the strips of a TIFF, staged to HBM as raw file bytes,
+// become sample planes on the device.
+//
+// The reference decodes with cv2.imread (libtiff + zlib, one core).  A TIFF
+// strip is an independent unit -- raw bytes, or its own zlib stream -- so the
+// strips of a band are decoded in parallel:
+//  * strips_copy_kernel: uncompressed strips, one CTA per strip (16-byte
+//    vector copies when aligned);
+//  * inflate_kernel: deflate strips (Compression 8 / 32946), one thread per
+//    zlib stream: RFC 1951 stored / fixed / dynamic blocks, canonical Huffman
+//    decoding by code length (count/symbol tables per stream), back-references
+//    from the stream's own output, Adler-32 verified;
+//  * unpredict_kernel: TIFF Predictor 2 (horizontal differencing) undone per
+//    row and channel, after an optional byte swap of big-endian ('MM') 16-bit
+//    samples.
+// A stream whose data is malformed, too short or too long sets its status
+// word (and the caller raises DataError, as cv2.imread failing does).
+#include "common.cuh"
+
+namespace ut {
+namespace {
+
+__constant__ uint16_t c_len_base[29] = {3,  4,  5,  6,  7,  8,  9,  10, 11,  13,  15,  17,  19,  23, 27,
+                                        31, 35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
+__constant__ uint8_t c_len_extra[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2,
+                                        2, 3, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 0};
+__constant__ uint16_t c_dist_base[30] = {1,    2,    3,    4,    5,    7,     9,     13,    17,  25,
+                                         33,   49,   65,   97,   129,  193,   257,   385,   513, 769,
+                                         1025, 1537, 2049, 3073, 4097, 6145,  8193,  12289, 16385, 24577};
+__constant__ uint8_t c_dist_extra[30] = {0, 0, 0, 0, 1, 1, 2, 2,  3,  3,  4,  4,  5,  5,  6,
+                                         6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
+
+struct Huff {
+  int16_t count[16];    // codes of each length
+  int16_t symbol[288];  // symbols in canonical order
+};
+
+// canonical tables from code lengths; < 0 if over-subscribed
+__device__ int build_huff(Huff* h, const uint8_t* length, int n) {
+  for (int l = 0; l < 16; ++l) h->count[l] = 0;
+  for (int i = 0; i < n; ++i) h->count[length[i]]++;
+  if (h->count[0] == n) return 0;
+  int left = 1;
+  for (int l = 1; l < 16; ++l) {
+    left <<= 1;
+    left -= h->count[l];
+    if (left < 0) return -1;
+  }
+  int16_t offs[16];
+  offs[1] = 0;
+  for (int l = 1; l < 15; ++l) offs[l + 1] = offs[l] + h->count[l];
+  for (int i = 0; i < n; ++i)
+    if (length[i]) h->symbol[offs[length[i]]++] = (int16_t)i;
+  return left;
+}
+
+struct BitIn {
+  const uint8_t* p;
+  const uint8_t* end;
+  uint64_t buf;
+  int cnt;
+  int over;  // bytes read past the end (zeros)
+};
+
+__device__ __forceinline__ void refill(BitIn& s) {
+  while (s.cnt <= 56) {
+    uint64_t b = 0;
+    if (s.p < s.end) b = *s.p++;
+    else ++s.over;
+    s.buf |= b << s.cnt;
+    s.cnt += 8;
+  }
+}
+__device__ __forceinline__ uint32_t getbits(BitIn& s, int n) {
+  if (s.cnt < n) refill(s);
+  const uint32_t v = (uint32_t)(s.buf & ((1ull << n) - 1));
+  s.buf >>= n;
+  s.cnt -= n;
+  return v;
+}
+// Huffman codes are packed MSB first: walk lengths 1..15
+__device__ __forceinline__ int decode_sym(BitIn& s, const Huff* h) {
+  if (s.cnt < 15) refill(s);
+  uint64_t bits = s.buf;
+  int code = 0, first = 0, index = 0;
+  for (int len = 1; len < 16; ++len) {
+    code |= (int)(bits & 1);
+    bits >>= 1;
+    const int count = h->count[len];
+    if (code - count < first) {
+      s.buf >>= len;
+      s.cnt -= len;
+      return h->symbol[index + (code - first)];
+    }
+    index += count;
+    first += count;
+    first <<= 1;
+    code <<= 1;
+  }
+  return -1;
+}
+
+enum { kBad = 1, kShort = 2, kLong = 3, kAdler = 4, kHeader = 5 };
+
+// One zlib stream -> out[0, out_len); returns 0 or an error code.
+__device__ int inflate_one(const uint8_t* in, int64_t in_len, uint8_t* out, int64_t out_len) {
+  if (in_len < 2) return kHeader;
+  const uint32_t cmf = in[0], flg = in[1];
+  if ((cmf & 15) != 8 || (cmf >> 4) > 7 || ((cmf << 8) | flg) % 31 != 0 || (flg & 0x20)) return kHeader;
+  BitIn s{in + 2, in + in_len, 0, 0, 0};
+  Huff lencode, distcode;
+  uint8_t lengths[320];
+  int64_t o = 0;
+  int last;
+  do {
+    last = (int)getbits(s, 1);
+    const int type = (int)getbits(s, 2);
+    if (type == 0) {  // stored: to a byte boundary, LEN, NLEN, bytes
+      const int drop = s.cnt & 7;
+      s.buf >>= drop;
+      s.cnt -= drop;
+      const uint32_t len = getbits(s, 16), nlen = getbits(s, 16);
+      if ((len ^ 0xFFFFu) != nlen) return kBad;
+      if (o + len > out_len) return kLong;
+      uint32_t k = 0;
+      while (k < len && s.cnt >= 8) {  // bytes still in the bit buffer
+        out[o++] = (uint8_t)s.buf;
+        s.buf >>= 8;
+        s.cnt -= 8;
+        ++k;
+      }
+      if (s.p + (len - k) > s.end) return kShort;
+      for (; k < len; ++k) out[o++] = *s.p++;
+      continue;
+    }
+    if (type == 3) return kBad;
+    if (type == 1) {
+      for (int i = 0; i < 144; ++i) lengths[i] = 8;
+      for (int i = 144; i < 256; ++i) lengths[i] = 9;
+      for (int i = 256; i < 280; ++i) lengths[i] = 7;
+      for (int i = 280; i < 288; ++i) lengths[i] = 8;
+      build_huff(&lencode, lengths, 288);
+      for (int i = 0; i < 30; ++i) lengths[i] = 5;
+      build_huff(&distcode, lengths, 30);
+    } else {
+      const int nlen = (int)getbits(s, 5) + 257, ndist = (int)getbits(s, 5) + 1;
+      const int ncode = (int)getbits(s, 4) + 4;
+      if (nlen > 286 || ndist > 30) return kBad;
+      const uint8_t order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+      for (int i = 0; i < 19; ++i) lengths[i] = 0;
+      for (int i = 0; i < ncode; ++i) lengths[order[i]] = (uint8_t)getbits(s, 3);
+      if (build_huff(&lencode, lengths, 19) != 0) return kBad;  // must be complete
+      int i = 0;
+      while (i < nlen + ndist) {
+        int sym = decode_sym(s, &lencode);
+        if (sym < 0) return kBad;
+        if (sym < 16) {
+          lengths[i++] = (uint8_t)sym;
+          continue;
+        }
+        int len = 0, rep;
+        if (sym == 16) {
+          if (i == 0) return kBad;
+          len = lengths[i - 1];
+          rep = 3 + (int)getbits(s, 2);
+        } else if (sym == 17) {
+          rep = 3 + (int)getbits(s, 3);
+        } else {
+          rep = 11 + (int)getbits(s, 7);
+        }
+        if (i + rep > nlen + ndist) return kBad;
+        while (rep--) lengths[i++] = (uint8_t)len;
+      }
+      if (lengths[256] == 0) return kBad;
+      const int el = build_huff(&lencode, lengths, nlen);
+      if (el < 0 || (el > 0 && nlen - lencode.count[0] != 1)) return kBad;
+      const int ed = build_huff(&distcode, lengths + nlen, ndist);
+      if (ed < 0 || (ed > 0 && ndist - distcode.count[0] != 1)) return kBad;
+    }
+    for (;;) {
+      int sym = decode_sym(s, &lencode);
+      if (sym < 0) return kBad;
+      if (sym < 256) {
+        if (o >= out_len) return kLong;
+        out[o++] = (uint8_t)sym;
+        continue;
+      }
+      if (sym == 256) break;
+      sym -= 257;
+      if (sym >= 29) return kBad;
+      const int len = c_len_base[sym] + (int)getbits(s, c_len_extra[sym]);
+      const int dsym = decode_sym(s, &distcode);
+      if (dsym < 0 || dsym >= 30) return kBad;
+      const int64_t dist = c_dist_base[dsym] + (int)getbits(s, c_dist_extra[dsym]);
+      if (dist > o) return kBad;
+      if (o + len > out_len) return kLong;
+      const uint8_t* from = out + o - dist;
+      for (int k = 0; k < len; ++k) out[o + k] = from[k];
+      o += len;
+    }
+  } while (!last);
+  if (o != out_len) return kShort;
+  // Adler-32 trailer (big-endian) after the last block, byte aligned
+  const int drop = s.cnt & 7;
+  s.buf >>= drop;
+  s.cnt -= drop;
+  uint32_t want = 0;
+  for (int k = 0; k < 4; ++k) want = (want << 8) | getbits(s, 8);
+  if (s.over > 8) return kShort;
+  uint32_t a = 1, b = 0;
+  for (int64_t k = 0; k < out_len; ++k) {
+    a += out[k];
+    if (a >= 65521u) a -= 65521u;
+    b += a;
+    if (b >= 65521u) b -= 65521u;
+  }
+  return ((b << 16) | a) == want ? 0 : kAdler;
+}
+
+__global__ void __launch_bounds__(64) inflate_kernel(const uint8_t* __restrict__ src, const int64_t* in_off,
+                                                     const int64_t* in_len, int64_t n, uint8_t* dst,
+                                                     const int64_t* out_off, const int64_t* out_len,
+                                                     int32_t* status) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  status[i] = inflate_one(src + in_off[i], in_len[i], dst + out_off[i], out_len[i]);
+}
+
+__global__ void __launch_bounds__(256) strips_copy_kernel(const uint8_t* __restrict__ src, const int64_t* in_off,
+                                                          const int64_t* in_len, uint8_t* dst,
+                                                          const int64_t* out_off, const int64_t* out_len,
+                                                          int32_t* status) {
+  const int64_t i = blockIdx.x;
+  const int64_t n = out_len[i];
+  if (threadIdx.x == 0) status[i] = in_len[i] < n ? kShort : 0;
+  const uint8_t* s = src + in_off[i];
+  uint8_t* d = dst + out_off[i];
+  const int64_t m = in_len[i] < n ? in_len[i] : n;
+  if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0) {
+    const int64_t v = m >> 4;
+    for (int64_t k = threadIdx.x; k < v; k += blockDim.x)
+      reinterpret_cast<uint4*>(d)[k] = reinterpret_cast<const uint4*>(s)[k];
+    for (int64_t k = (v << 4) + threadIdx.x; k < m; k += blockDim.x) d[k] = s[k];
+  } else {
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) d[k] = s[k];
+  }
+}
+
+template <typename T>
+__global__ void unpredict_kernel(T* img, int64_t rows, int64_t spr, int ch, int predictor, int swap) {
+  const int64_t y = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (y >= rows) return;
+  T* row = img + y * spr;
+  if (swap && sizeof(T) == 2)
+    for (int64_t x = 0; x < spr; ++x) {
+      const uint16_t v = (uint16_t)row[x];
+      row[x] = (T)((v >> 8) | (v << 8));
+    }
+  if (predictor == 2)
+    for (int64_t x = ch; x < spr; ++x) row[x] = (T)(row[x] + row[x - ch]);
+}
+
+}  // namespace
+}  // namespace ut
+
+using namespace ut;
+
+extern "C" {
+
+int ut_decode_strips(const uint8_t* src, const int64_t* in_off, const int64_t* in_len, int64_t nstrips,
+                     int32_t compression, uint8_t* dst, const int64_t* out_off, const int64_t* out_len,
+                     int32_t* status, void* stream) {
+  UT_REQUIRE(nstrips >= 0, "negative strip count");
+  UT_REQUIRE(compression == 1 || compression == 8,
+             "strip compression must be 1 (none) or 8 (zlib deflate), got %d", compression);
+  if (nstrips == 0) return UT_OK;
+  UT_REQUIRE(src && in_off && in_len && dst && out_off && out_len && status, "ut_decode_strips: null pointer");
+  cudaStream_t st = as_stream(stream);
+  if (compression == 1) {
+    strips_copy_kernel<<<(unsigned)nstrips, 256, 0, st>>>(src, in_off, in_len, dst, out_off, out_len, status);
+    UT_CHECK_LAUNCH("strips_copy_kernel");
+  } else {
+    inflate_kernel<<<(unsigned)((nstrips + 63) / 64), 64, 0, st>>>(src, in_off, in_len, nstrips, dst, out_off,
+                                                                   out_len, status);
+    UT_CHECK_LAUNCH("inflate_kernel");
+  }
+  return UT_OK;
+}
+
+int ut_unpredict(void* img, int32_t depth, int64_t rows, int64_t cols, int32_t channels, int32_t predictor,
+                 int32_t swap_bytes, void* stream) {
+  UT_REQUIRE(depth == 8 || depth == 16, "sample depth must be 8 or 16, got %d", depth);
+  UT_REQUIRE(predictor == 1 || predictor == 2, "TIFF predictor must be 1 or 2, got %d", predictor);
+  UT_REQUIRE(rows >= 0 && cols >= 0 && channels >= 1, "bad image geometry");
+  if (rows == 0 || cols == 0 || (predictor == 1 && !(swap_bytes && depth == 16))) return UT_OK;
+  cudaStream_t st = as_stream(stream);
+  const unsigned grid = (unsigned)((rows + 127) / 128);
+  if (depth == 8)
+    unpredict_kernel<uint8_t><<<grid, 128, 0, st>>>(static_cast<uint8_t*>(img), rows, cols * channels,
+                                                    channels, predictor, 0);
+  else
+    unpredict_kernel<uint16_t><<<grid, 128, 0, st>>>(static_cast<uint16_t*>(img), rows, cols * channels,
+                                                     channels, predictor, swap_bytes);
+  UT_CHECK_LAUNCH("unpredict_kernel");
+  return UT_OK;
+}
+
+}  // extern "C"

@@ -185,3 +185,127 @@ def save_image(img, path: str | Path, compression: str = "none") -> None:
         path.write_bytes(data)
     except OSError as e:
         raise DataError(f"failed to write image {path}: {e}") from None
+
+
+# ------------------------------------------------------------------ decode
+
+_TIFF_TYPES = {1: ("B", 1), 3: ("H", 2), 4: ("I", 4), 16: ("Q", 8)}
+
+
+class _Unsupported(Exception):
+    """A file layout the device decoder does not handle (the caller uses cv2)."""
+
+
+def _tiff_layout(data: bytes) -> dict:
+    """Parse the first IFD of a classic TIFF (host, header bytes only)."""
+    if len(data) < 8 or data[:2] not in (b"II", b"MM"):
+        raise _Unsupported("not a TIFF")
+    bo = "<" if data[:2] == b"II" else ">"
+    magic, ifd = struct.unpack(bo + "HI", data[2:8])
+    if magic != 42:
+        raise _Unsupported("not a classic TIFF")
+    (n,) = struct.unpack(bo + "H", data[ifd:ifd + 2])
+    tags = {}
+    for i in range(n):
+        tag, typ, count = struct.unpack(bo + "HHI", data[ifd + 2 + 12 * i:ifd + 10 + 12 * i])
+        if typ not in _TIFF_TYPES:
+            continue
+        code, size = _TIFF_TYPES[typ]
+        raw_at = ifd + 10 + 12 * i
+        if size * count > 4:
+            (raw_at,) = struct.unpack(bo + "I", data[raw_at:raw_at + 4])
+        tags[tag] = list(struct.unpack(bo + code * count, data[raw_at:raw_at + size * count]))
+    get = lambda t, d=None: tags.get(t, [d])  # noqa: E731
+    lay = {
+        "bo": bo, "width": get(256)[0], "height": get(257)[0], "bps": get(258, 1),
+        "compression": get(259, 1)[0], "photometric": get(262, 1)[0], "spp": get(277, 1)[0],
+        "rps": get(278, 2 ** 32 - 1)[0], "planar": get(284, 1)[0], "predictor": get(317, 1)[0],
+        "format": get(339, 1)[0], "offsets": tags.get(273), "counts": tags.get(279),
+    }
+    if 322 in tags or lay["offsets"] is None or lay["counts"] is None:
+        raise _Unsupported("tiled or strip-less TIFF")
+    if lay["compression"] not in (1, 8, 32946) or lay["predictor"] not in (1, 2):
+        raise _Unsupported(f"compression {lay['compression']} / predictor {lay['predictor']}")
+    if len(set(lay["bps"])) != 1 or lay["bps"][0] not in (8, 16) or lay["format"] != 1:
+        raise _Unsupported("sample type")
+    if lay["spp"] not in (1, 3) or (lay["spp"] == 3 and lay["planar"] != 1):
+        raise _Unsupported("sample layout")
+    if lay["photometric"] not in ((1,) if lay["spp"] == 1 else (2,)):
+        raise _Unsupported(f"photometric {lay['photometric']}")
+    return lay
+
+
+def decode_tiff(data: bytes, device=None) -> torch.Tensor:
+    """Device (H, W[, 3]) uint8 / uint16 planes of a stripped TIFF (raw or
+    deflate, Predictor 1 / 2, either byte order).  Raises _Unsupported for
+    other layouts."""
+    lay = _tiff_layout(data)
+    device = device or dev.require_cuda()
+    h, w, ch = int(lay["height"]), int(lay["width"]), int(lay["spp"])
+    depth = int(lay["bps"][0])
+    rb = w * ch * depth // 8
+    rps = min(int(lay["rps"]), h)
+    nstrips = -(-h // rps)
+    offs = np.asarray(lay["offsets"], dtype=np.int64)
+    counts = np.asarray(lay["counts"], dtype=np.int64)
+    if len(offs) != nstrips or len(counts) != nstrips:
+        raise DataError(f"TIFF lists {len(offs)} strips, expected {nstrips}")
+    if int((offs + counts).max()) > len(data):
+        raise DataError("TIFF strip runs past the end of the file")
+    out_len = np.full(nstrips, rps * rb, dtype=np.int64)
+    out_len[-1] = (h - (nstrips - 1) * rps) * rb
+    out_off = np.arange(nstrips, dtype=np.int64) * rps * rb
+    dtype = torch.uint8 if depth == 8 else torch.uint16
+    out = torch.empty((h, w, ch), dtype=dtype, device=device)
+    with torch.cuda.device(device):
+        src = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(device)
+        tables = torch.from_numpy(np.stack([offs, counts, out_off, out_len])).to(device)
+        status = torch.empty(nstrips, dtype=torch.int32, device=device)
+        L = _lib.lib()
+        s = dev.stream_handle()
+        code = 1 if lay["compression"] == 1 else 8
+        _lib.check(L.ut_decode_strips(src.data_ptr(), tables[0].data_ptr(), tables[1].data_ptr(),
+                                      nstrips, code, out.data_ptr(), tables[2].data_ptr(),
+                                      tables[3].data_ptr(), status.data_ptr(), s),
+                   "ut_decode_strips")
+        _lib.check(L.ut_unpredict(out.data_ptr(), depth, h, w, ch, int(lay["predictor"]),
+                                  int(lay["bo"] == ">" and depth == 16), s), "ut_unpredict")
+        bad = int((status != 0).sum().item())
+    if bad:
+        raise DataError(f"TIFF has {bad} undecodable strip(s)")
+    return out if ch == 3 else out.view(h, w)
+
+
+def read_image_device(path: str | Path, device=None):
+    """(device tensor, decoded-on-device flag) for an image file: stripped
+    TIFFs decode on the B200; other files (PNG, LZW / tiled TIFF, ...) go
+    through cv2.imread on the host exactly as the reference reads them, then
+    to the device.  DataError if the file cannot be read."""
+    path = Path(path)
+    try:
+        data = path.read_bytes()
+    except OSError:
+        raise DataError(f"cannot read image {path}") from None
+    try:
+        return decode_tiff(data, device), True
+    except _Unsupported:
+        pass
+    import cv2  # the reference's decoder, for layouts the device path does not parse
+
+    img = cv2.imdecode(np.frombuffer(data, dtype=np.uint8), cv2.IMREAD_UNCHANGED)
+    if img is None:
+        raise DataError(f"cannot read image {path}")
+    if img.ndim == 3 and img.shape[2] == 3:
+        img = img[:, :, ::-1]  # BGR -> RGB
+    return dev.to_device(np.ascontiguousarray(img), device or dev.require_cuda()), False
+
+
+def load_image(path: str | Path) -> np.ndarray:
+    """Read a TIFF or PNG back as uint8/uint16, RGB channel order
+    (rendering.py:334-343)."""
+    t, _ = read_image_device(path)
+    if t.dim() == 3 and t.shape[2] != 3:
+        raise DataError(f"{path}: expected 3 channels, got {t.shape[2]}")
+    img = t.cpu().numpy()
+    check_image(img)
+    return np.ascontiguousarray(img)

@@ -17,6 +17,7 @@ import threading
 import warnings
 import weakref
 from dataclasses import dataclass, field
+from pathlib import Path
 
 import numpy as np
 import torch
@@ -156,11 +157,17 @@ def on_device(stack) -> DeviceStack:
                 hit[1].planes.device == device and hit[1].normalized == stack.normalized:
             return hit[1]
     ds = DeviceStack.from_host(stack, device)
+    _register_device_copy(stack, ds)
+    return ds
+
+
+def _register_device_copy(stack: SpectralStack, ds: DeviceStack) -> None:
+    """Remember ``ds`` as the HBM copy of the host stack's (immutable) planes."""
+    key = id(stack.planes)
     with _cache_lock:
         ref = weakref.ref(stack.planes, lambda _r, k=key: _device_copies.pop(k, None)) \
             if _weakrefable(stack.planes) else (lambda: None)
         _device_copies[key] = (ref, ds)
-    return ds
 
 
 def _weakrefable(a) -> bool:
@@ -214,3 +221,94 @@ def normalize_stack(stack, scope: str = "per-band"):
     if host:
         return SpectralStack(stack.bands, out.cpu().numpy(), 8, normalized=True)
     return DeviceStack(ds.bands, out, 8, True, ds.row0, ds.full_height)
+
+
+# ------------------------------------------------------------------ load_stack
+
+def _parse_manifest_line(line: str, lineno: int, base: Path):
+    """``path,wavelength_nm,illumination[,filter]`` (stack.py:101-116)."""
+    parts = [p.strip() for p in line.split(",")]
+    if len(parts) not in (3, 4):
+        raise DataError(f"manifest line {lineno}: expected "
+                        f"'path,wavelength_nm,illumination[,filter]', got {line!r}")
+    path = base / parts[0]
+    try:
+        wavelength = float(parts[1])
+    except ValueError:
+        raise DataError(f"manifest line {lineno}: bad wavelength {parts[1]!r}") from None
+    filt = parts[3] if len(parts) == 4 else None
+    return path, wavelength, parts[2], filt
+
+
+def load_device_stack(manifest) -> DeviceStack:
+    """The bands named by a manifest, decoded into one HBM cube (stripped TIFF
+    bands decode on the device; see image_io.read_image_device)."""
+    from .image_io import read_image_device
+
+    manifest = Path(manifest)
+    if not manifest.is_file():
+        raise DataError(f"manifest not found: {manifest}")
+    entries = []
+    for lineno, raw in enumerate(manifest.read_text(encoding="utf-8").splitlines(), 1):
+        line = raw.strip()
+        if not line or line.startswith("#"):
+            continue
+        entries.append(_parse_manifest_line(line, lineno, manifest.parent))
+    if not entries:
+        raise DataError(f"manifest {manifest} lists no bands")
+    metas, planes = [], []
+    shape, depth = None, None
+    for band_id, (path, wavelength, illum, filt) in enumerate(entries):
+        if not path.is_file():
+            raise DataError(f"band {band_id}: image file not found: {path}")
+        try:
+            img, _ = read_image_device(path)
+        except DataError:
+            raise DataError(f"band {band_id}: could not decode {path}") from None
+        if img.dim() != 2:
+            raise DataError(f"band {band_id}: {path} has {img.shape[2]} channels; "
+                            f"stacks are built from single-channel images")
+        if img.dtype == torch.uint8:
+            band_depth = 8
+        elif img.dtype == torch.uint16:
+            band_depth = 16
+        else:
+            raise DataError(f"band {band_id}: {path} has unsupported sample type {img.dtype}")
+        if shape is None:
+            shape, depth = tuple(img.shape), band_depth
+        else:
+            if tuple(img.shape) != shape:
+                raise DataError(f"band {band_id}: size {img.shape[1]}x{img.shape[0]} does not "
+                                f"match band 0 ({shape[1]}x{shape[0]})")
+            if band_depth != depth:
+                raise DataError(f"band {band_id}: {band_depth}-bit plane in a {depth}-bit stack")
+        metas.append(BandMeta(band_id, wavelength, illum, filt))
+        planes.append(img)
+    return DeviceStack(tuple(metas), torch.stack(planes), depth, False)
+
+
+def load_stack(manifest) -> SpectralStack:
+    """Load a stack from a manifest file (stack.py:119-177): one band per line,
+    ``relative/path.tif,wavelength_nm,illumination[,filter]``, ``#`` comments,
+    paths relative to the manifest, band ids in manifest order; every band a
+    single-channel image of one shared size and bit depth.  The bands are
+    decoded on the device; the returned host stack keeps that HBM copy
+    registered, so the fit / projection that follows pays no upload."""
+    ds = load_device_stack(manifest)
+    host = SpectralStack(ds.bands, ds.planes.cpu().numpy(), ds.bit_depth, False)
+    _register_device_copy(host, ds)
+    return host
+
+
+def crop(stack, x0: int, y0: int, width: int, height: int):
+    """Crop all bands identically to the given rectangle (stack.py:216-225);
+    a DeviceStack is cropped in HBM."""
+    if width <= 0 or height <= 0:
+        raise DataError(f"crop rectangle has zero area: {width}x{height}")
+    if x0 < 0 or y0 < 0 or x0 + width > stack.width or y0 + height > stack.height:
+        raise DataError(f"crop ({x0},{y0},{width},{height}) outside "
+                        f"{stack.width}x{stack.height} stack")
+    planes = stack.planes[:, y0:y0 + height, x0:x0 + width]
+    if isinstance(stack, DeviceStack):
+        return DeviceStack(stack.bands, planes.contiguous(), stack.bit_depth, stack.normalized)
+    return SpectralStack(stack.bands, planes.copy(), stack.bit_depth, stack.normalized)

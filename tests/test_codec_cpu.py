@@ -89,3 +89,33 @@ def test_render_names_and_recipe_validation(tmp_path):
         ut.render_planes(None, None, [spec], tmp_path, fmt="jpg")
     with pytest.raises(DataError, match="spec"):
         ut.render_planes(None, None, [], tmp_path)
+
+
+def test_manifest_errors_before_any_decode(tmp_path):
+    """load_stack's manifest checks (test_stack.py:86-113) need no device."""
+    import paper_1612_06457_b200 as ut
+
+    def manifest(lines):
+        p = tmp_path / "m.txt"
+        p.write_text("\n".join(lines) + "\n", encoding="utf-8")
+        return p
+
+    with pytest.raises(DataError, match="gone.tif"):
+        ut.load_stack(manifest(["gone.tif,365,uv"]))
+    with pytest.raises(DataError, match="line 2"):
+        ut.load_stack(manifest(["# header", "not enough fields"]))
+    with pytest.raises(DataError):
+        ut.load_stack(manifest(["# nothing"]))
+    with pytest.raises(DataError, match="manifest not found"):
+        ut.load_stack(tmp_path / "absent.txt")
+
+
+def test_tiff_layout_parse():
+    """Host IFD parsing of a device-style TIFF (framing only)."""
+    img = np.arange(6 * 5, dtype=np.uint16).reshape(6, 5)
+    data = image_io._tiff_file(img.tobytes(), np.array([img.nbytes]), 6, 5, 1, 16, 1, 6)
+    lay = image_io._tiff_layout(data)
+    assert (lay["width"], lay["height"], lay["bps"], lay["compression"]) == (5, 6, [16], 1)
+    assert lay["offsets"] == [8] and lay["counts"] == [img.nbytes]
+    with pytest.raises(image_io._Unsupported):
+        image_io._tiff_layout(b"\x89PNG\r\n\x1a\n")
