@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-stream-e2e", action="store_true", help="serial e2e only")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-pca", action="store_true",
+                    help="skip the PCA companion measurement on the same cube")
     ap.add_argument("--folios", type=int, default=64, help="cfg5: folios in the batch")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target CPU work for the cpu_baseline sample")
@@ -348,6 +350,50 @@ def run_folios(args):
     return 0
 
 
+def pca_companion(ut, stack, cfg, args, group, world, stream):
+    import torch
+
+    pipe = ut.PcaPipeline(stack, k=cfg.k, precision=args.precision, group=group)
+    for _ in range(3):
+        pipe.run()
+    torch.cuda.synchronize()
+    pipe.check()
+    steps = max(3, min(args.steps, 20))
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    for e in ev:
+        e[0].record(stream)
+        pipe.fit_only()
+        e[1].record(stream)
+        pipe.project_kernel()
+        e[2].record(stream)
+        pipe.reduce_minmax(pipe.minmax)
+        pipe.stretch_only()
+        e[3].record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    pipe.check()
+    ms = max_over_ranks(float(np.mean([e[0].elapsed_time(e[3]) for e in ev])), world)
+    fit_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+    k4_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    tail_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
+    per_px = 2 * cfg.bands * cfg.sample_bytes + cfg.k       # PCA 2*B*s + K
+    peak, _ = hbm_peak()
+    step_gbs = per_px * stack.pixels / (ms * 1e-3) / 1e9
+    out = {"metric": "PCA Mpixel/s (covariance+eigen+projection)",
+           "workload": cfg.name.replace("_cva_", "_pca_"),
+           "value": round(cfg.pixels / (ms * 1e-3) / 1e6, 3), "unit": "Mpixel/s",
+           "ms_per_step": round(ms, 4), "steps": steps,
+           "split_ms": {"fit": round(fit_ms, 4), "project": round(k4_ms, 4),
+                        "minmax+stretch": round(tail_ms, 4)},
+           "roofline_step": {"bytes_per_px": per_px, "achieved": round(step_gbs, 1),
+                             "frac": round(step_gbs / peak, 4)}}
+    del pipe
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_b200(args):
     import torch
 
@@ -443,6 +489,13 @@ def run_b200(args):
                 traffic = round(ent["bytes_per_pixel"] * local_px / 1e9, 3)
         except Exception:
             traffic = None
+
+    # ---- PCA companion (north-star second path): the unsupervised PCA step on
+    # the same resident cube (cfg 4's generator, so this is the cfg4pca
+    # workload): covariance (K2) + eigen + projection (K4) + stretch (K5)
+    pca = None
+    if cfg.method == "cva" and not args.no_pca:
+        pca = pca_companion(ut, stack, cfg, args, group, world, stream)
 
     # ---- e2e: host (pinned) cube in, uint8 planes out, through the same API
     e2e = None
@@ -555,6 +608,7 @@ def run_b200(args):
                                            "minmax+stretch": round(tail_ms, 4)}},
             "clocks": clocks.summary(),
             "e2e": e2e,
+            "pca": pca,
             "gpu_launches": launches,
             "cpu_baseline": cpu,
         }
