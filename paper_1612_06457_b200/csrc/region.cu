@@ -80,59 +80,49 @@ __device__ __forceinline__ const T* pixel_ptr(const Region& r, int64_t pix) {
   return static_cast<const T*>(r.data) + (r.y0 + y) * r.rs + r.x0 + x;
 }
 
-// shift_b = mean of up to 4096 pixels at a fixed stride (one CTA, fixed tree)
+// shift_b = mean of up to 4096 pixels at a fixed stride, one CTA per band (the
+// strided samples are scattered over the cube, so the loads of all bands go out
+// at once); each thread keeps its <= 4 samples in registers for the spread
+// pass.  Fixed reduction order: per thread, xor tree per warp, warps in order.
 template <typename T>
 __global__ void __launch_bounds__(1024) shift_kernel(Region r, RegionWs ws) {
-  __shared__ double red[1024 / 32][kMaxBands];
+  constexpr int kPer = kSample / 1024;
+  __shared__ double red[32];
+  __shared__ double mean_sh;
+  const int b = blockIdx.x;
   const int64_t count = r.npix < kSample ? r.npix : kSample;
   const int64_t step = r.npix / count;
-  double acc[kMaxBands];
+  double v[kPer];
+  double acc = 0.0;
 #pragma unroll
-  for (int b = 0; b < kMaxBands; ++b) acc[b] = 0.0;
-  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) {
-    const T* p = pixel_ptr<T>(r, i * step);
-#pragma unroll
-    for (int b = 0; b < kMaxBands; ++b)
-      if (b < r.bands) acc[b] += to_f64(p[b * r.bs]);
+  for (int u = 0; u < kPer; ++u) {
+    const int64_t i = threadIdx.x + (int64_t)u * 1024;
+    v[u] = i < count ? to_f64(pixel_ptr<T>(r, i * step)[b * r.bs]) : 0.0;
+    acc += v[u];
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int b = 0; b < kMaxBands; ++b) {
-    double v = acc[b];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[warp][b] = v;
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 32; ++w) t += red[w];
+    mean_sh = t / (double)count;
   }
   __syncthreads();
-  __shared__ double mean[kMaxBands];
-  if (threadIdx.x < r.bands) {
-    double v = 0.0;
-    for (int w = 0; w < 32; ++w) v += red[w][threadIdx.x];
-    mean[threadIdx.x] = v / (double)count;
-  }
-  __syncthreads();
+  const double m = mean_sh;
   // spread of the sample around it: sets the integer path's fixed-point grid
-  double dev[kMaxBands];
+  double dev = 0.0;
 #pragma unroll
-  for (int b = 0; b < kMaxBands; ++b) dev[b] = 0.0;
-  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) {
-    const T* p = pixel_ptr<T>(r, i * step);
-#pragma unroll
-    for (int b = 0; b < kMaxBands; ++b)
-      if (b < r.bands) dev[b] = fmax(dev[b], fabs(to_f64(p[b * r.bs]) - mean[b]));
-  }
+  for (int u = 0; u < kPer; ++u)
+    if (threadIdx.x + (int64_t)u * 1024 < count) dev = fmax(dev, fabs(v[u] - m));
+  for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
   __syncthreads();
-#pragma unroll
-  for (int b = 0; b < kMaxBands; ++b) {
-    double v = dev[b];
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) red[warp][b] = v;
-  }
+  if (lane == 0) red[warp] = dev;
   __syncthreads();
-  if (threadIdx.x < r.bands) {
-    const int b = threadIdx.x;
+  if (threadIdx.x == 0) {
     double d = 0.0;
-    for (int w = 0; w < 32; ++w) d = fmax(d, red[w][b]);
-    const double m = mean[b];
+    for (int w = 0; w < 32; ++w) d = fmax(d, red[w]);
     // Fixed-point grid 2^-f: |x - s| <= 4 * (sample spread) maps inside +-2^30, so
     // samples up to ~8x the sampled spread fit the 32-bit range (else the
     // integer path flags the region and the fp64 path redoes it); integer
@@ -151,8 +141,8 @@ __global__ void __launch_bounds__(1024) shift_kernel(Region r, RegionWs ws) {
     ws.scale[b] = sc;
     ws.addend[b] = (0x1.8p52 - S) + 2155905152.0;  // + 0x80808080 (balanced digits)
     ws.shift[b] = ldexp(S, -f);
+    if (b == 0) *ws.flag = 0;
   }
-  if (threadIdx.x == 0) *ws.flag = 0;
 }
 
 template <typename T>
@@ -925,7 +915,7 @@ static_assert(148 * kImRec <= kMaxG * kEnt, "integer partials must fit the regio
 
 template <typename T>
 int launch_region_imma(const Region& r, RegionWs ws, double* moments, int G, cudaStream_t st) {
-  shift_kernel<T><<<1, 1024, 0, st>>>(r, ws);
+  shift_kernel<T><<<r.bands, 1024, 0, st>>>(r, ws);
   UT_CHECK_LAUNCH("shift_kernel");
   ImParams ip;
   ip.data = static_cast<const T*>(r.data) + r.y0 * r.rs + r.x0;
@@ -982,7 +972,7 @@ template <typename T>
 int launch_region_dmma(const Region& r, RegionWs ws, double* moments, cudaStream_t st,
                        const int* gate = nullptr) {
   if (!gate) {
-    shift_kernel<T><<<1, 1024, 0, st>>>(r, ws);
+    shift_kernel<T><<<r.bands, 1024, 0, st>>>(r, ws);
     UT_CHECK_LAUNCH("shift_kernel");
   }
   RdParams rp;
@@ -1026,7 +1016,7 @@ bool region_dmma_enabled() {
 
 template <typename T>
 int launch_region(Region r, RegionWs ws, double* moments, cudaStream_t st) {
-  shift_kernel<T><<<1, 1024, 0, st>>>(r, ws);
+  shift_kernel<T><<<r.bands, 1024, 0, st>>>(r, ws);
   UT_CHECK_LAUNCH("shift_kernel");
   region_kernel<T><<<r.G, kThreads, 0, st>>>(r, ws);
   UT_CHECK_LAUNCH("region_kernel");
