@@ -512,7 +512,10 @@ constexpr int kImOpP = UT_IM_OPP;         // pixels per operand buffer (MMAs of 
 constexpr int kImStagesOp = UT_IM_SOP;    // operand ring
 constexpr int kImProd = 4;                // producer warps (one thread's bulk copies issue slowly)
 constexpr int kImConv = kImP / 16;        // converter warps: one 16-pixel chunk of every tile
-constexpr int kImThreads = (kImProd + 1 + kImConv) * 32;
+#ifndef UT_IM_EPI_DED  // 1: four dedicated epilogue warps (converters never stop for a flush)
+#define UT_IM_EPI_DED 1
+#endif
+constexpr int kImThreads = (kImProd + 1 + kImConv + (UT_IM_EPI_DED ? 4 : 0)) * 32;
 constexpr int kImEpi = 8;                 // epilogue warps 8..11 (converters; warp % 4 = digit)
 static_assert(kImEpi >= kImProd + 1 && kImEpi + 4 <= kImProd + 1 + kImConv, "epilogue warps");
 constexpr int kImBars = 2 * kImStagesIn + 2 * kImStagesOp + 4;
@@ -724,7 +727,8 @@ region_imma_kernel(ImParams r) {
     // -------------------------------------------------- converters + epilogue
     // warp cw converts chunk cw (pixels 16 cw .. 16 cw + 15) of every tile; lane = band
     const int cw = warp - kImProd - 1;
-    const bool epi = warp >= kImEpi && warp < kImEpi + 4;
+    const bool ded = UT_IM_EPI_DED && warp >= kImProd + 1 + kImConv;  // dedicated epilogue
+    const bool epi = ded || (!UT_IM_EPI_DED && warp >= kImEpi && warp < kImEpi + 4);
     const int b = lane;
     const double scale = b < B ? r.scale[b] : 0.0;
     const double addend = b < B ? r.addend[b] : 0.0;
@@ -768,7 +772,10 @@ region_imma_kernel(ImParams r) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[a]);
     };
-    for (int i = 0; i < nloc; ++i) {
+    if (ded) {
+      for (int w = 0; nloc > 0 && w <= (nloc - 1) / kImWindowTiles; ++w) flush(w);
+    }
+    for (int i = 0; i < (ded ? 0 : nloc); ++i) {
       const int u = H * i + cw / CPB;
       const int st = i % kImStagesIn, o = u % kImStagesOp;
       im_wait(&in_full[st], (i / kImStagesIn) & 1);
@@ -826,14 +833,15 @@ region_imma_kernel(ImParams r) {
         mbar_arrive(&in_empty[st]);
         mbar_arrive(&op_full[o]);
       }
-      if (epi && (i % kImWindowTiles) == 0 && i >= kImWindowTiles) flush(i / kImWindowTiles - 1);
+      if (epi && !UT_IM_EPI_DED && (i % kImWindowTiles) == 0 && i >= kImWindowTiles)
+        flush(i / kImWindowTiles - 1);
     }
-    if (epi && nloc > 0) flush((nloc - 1) / kImWindowTiles);
+    if (epi && !UT_IM_EPI_DED && nloc > 0) flush((nloc - 1) / kImWindowTiles);
     if (bad) atomicOr(&bad_any, 1);
     double ds = dsum[0];
 #pragma unroll
     for (int q = 1; q < UT_IM_DSUM; ++q) ds += dsum[q];
-    xsum[cw][b] = ds;
+    if (!ded) xsum[cw][b] = ds;
   }
   tc_fence_before();
   __syncthreads();
