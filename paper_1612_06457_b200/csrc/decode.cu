@@ -64,6 +64,13 @@ struct BitIn {
 };
 
 __device__ __forceinline__ void refill(BitIn& s) {
+  if (s.cnt <= 32 && s.p + 4 <= s.end) {  // four bytes at once (independent loads)
+    const uint64_t w = (uint64_t)s.p[0] | ((uint64_t)s.p[1] << 8) | ((uint64_t)s.p[2] << 16) |
+                       ((uint64_t)s.p[3] << 24);
+    s.buf |= w << s.cnt;
+    s.cnt += 32;
+    s.p += 4;
+  }
   while (s.cnt <= 56) {
     uint64_t b = 0;
     if (s.p < s.end) b = *s.p++;
@@ -104,12 +111,12 @@ __device__ __forceinline__ int decode_sym(BitIn& s, const Huff* h) {
 enum { kBad = 1, kShort = 2, kLong = 3, kAdler = 4, kHeader = 5 };
 
 // One zlib stream -> out[0, out_len); returns 0 or an error code.
-__device__ int inflate_one(const uint8_t* in, int64_t in_len, uint8_t* out, int64_t out_len) {
+__device__ int inflate_one(const uint8_t* in, int64_t in_len, uint8_t* out, int64_t out_len,
+                           Huff& lencode, Huff& distcode) {
   if (in_len < 2) return kHeader;
   const uint32_t cmf = in[0], flg = in[1];
   if ((cmf & 15) != 8 || (cmf >> 4) > 7 || ((cmf << 8) | flg) % 31 != 0 || (flg & 0x20)) return kHeader;
   BitIn s{in + 2, in + in_len, 0, 0, 0};
-  Huff lencode, distcode;
   uint8_t lengths[320];
   int64_t o = 0;
   int last;
@@ -218,13 +225,18 @@ __device__ int inflate_one(const uint8_t* in, int64_t in_len, uint8_t* out, int6
   return ((b << 16) | a) == want ? 0 : kAdler;
 }
 
-__global__ void __launch_bounds__(64) inflate_kernel(const uint8_t* __restrict__ src, const int64_t* in_off,
-                                                     const int64_t* in_len, int64_t n, uint8_t* dst,
-                                                     const int64_t* out_off, const int64_t* out_len,
-                                                     int32_t* status) {
+// one thread per stream; its Huffman tables live in shared memory (the
+// decode loop reads them once per code bit)
+constexpr int kInfThreads = 32;
+__global__ void __launch_bounds__(kInfThreads) inflate_kernel(const uint8_t* __restrict__ src,
+                                                              const int64_t* in_off, const int64_t* in_len,
+                                                              int64_t n, uint8_t* dst, const int64_t* out_off,
+                                                              const int64_t* out_len, int32_t* status) {
+  __shared__ Huff tabs[2][kInfThreads];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  status[i] = inflate_one(src + in_off[i], in_len[i], dst + out_off[i], out_len[i]);
+  status[i] = inflate_one(src + in_off[i], in_len[i], dst + out_off[i], out_len[i],
+                          tabs[0][threadIdx.x], tabs[1][threadIdx.x]);
 }
 
 __global__ void __launch_bounds__(256) strips_copy_kernel(const uint8_t* __restrict__ src, const int64_t* in_off,
@@ -281,8 +293,8 @@ int ut_decode_strips(const uint8_t* src, const int64_t* in_off, const int64_t* i
     strips_copy_kernel<<<(unsigned)nstrips, 256, 0, st>>>(src, in_off, in_len, dst, out_off, out_len, status);
     UT_CHECK_LAUNCH("strips_copy_kernel");
   } else {
-    inflate_kernel<<<(unsigned)((nstrips + 63) / 64), 64, 0, st>>>(src, in_off, in_len, nstrips, dst, out_off,
-                                                                   out_len, status);
+    inflate_kernel<<<(unsigned)((nstrips + kInfThreads - 1) / kInfThreads), kInfThreads, 0, st>>>(
+        src, in_off, in_len, nstrips, dst, out_off, out_len, status);
     UT_CHECK_LAUNCH("inflate_kernel");
   }
   return UT_OK;

@@ -235,12 +235,9 @@ def _tiff_layout(data: bytes) -> dict:
     return lay
 
 
-def decode_tiff(data: bytes, device=None) -> torch.Tensor:
-    """Device (H, W[, 3]) uint8 / uint16 planes of a stripped TIFF (raw or
-    deflate, Predictor 1 / 2, either byte order).  Raises _Unsupported for
-    other layouts."""
+def _tiff_plan(data: bytes) -> dict:
+    """Geometry and strip tables of a device-decodable TIFF (host)."""
     lay = _tiff_layout(data)
-    device = device or dev.require_cuda()
     h, w, ch = int(lay["height"]), int(lay["width"]), int(lay["spp"])
     depth = int(lay["bps"][0])
     rb = w * ch * depth // 8
@@ -254,26 +251,65 @@ def decode_tiff(data: bytes, device=None) -> torch.Tensor:
         raise DataError("TIFF strip runs past the end of the file")
     out_len = np.full(nstrips, rps * rb, dtype=np.int64)
     out_len[-1] = (h - (nstrips - 1) * rps) * rb
-    out_off = np.arange(nstrips, dtype=np.int64) * rps * rb
-    dtype = torch.uint8 if depth == 8 else torch.uint16
-    out = torch.empty((h, w, ch), dtype=dtype, device=device)
+    return {"h": h, "w": w, "ch": ch, "depth": depth, "bytes": h * rb, "offs": offs,
+            "counts": counts, "out_off": np.arange(nstrips, dtype=np.int64) * rps * rb,
+            "out_len": out_len, "code": 1 if lay["compression"] == 1 else 8,
+            "predictor": int(lay["predictor"]), "swap": int(lay["bo"] == ">" and depth == 16)}
+
+
+def decode_tiff_batch(datas: list, device=None) -> list:
+    """Device planes of several stripped TIFFs (raw or deflate, Predictor 1 / 2,
+    either byte order) with one staging copy and one decode launch per
+    compression kind, so every strip of every file decodes in parallel.
+    Raises _Unsupported if any file has another layout."""
+    plans = [_tiff_plan(d) for d in datas]
+    device = device or dev.require_cuda()
+    file_base = np.cumsum([0] + [len(d) for d in datas])
+    out_base = np.cumsum([0] + [pl["bytes"] for pl in plans])
     with torch.cuda.device(device):
-        src = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(device)
-        tables = torch.from_numpy(np.stack([offs, counts, out_off, out_len])).to(device)
-        status = torch.empty(nstrips, dtype=torch.int32, device=device)
+        host = torch.empty(int(file_base[-1]), dtype=torch.uint8, pin_memory=True)
+        hv = host.numpy()
+        for d, b0 in zip(datas, file_base):
+            hv[b0:b0 + len(d)] = np.frombuffer(d, dtype=np.uint8)
+        src = host.to(device, non_blocking=True)
+        out = torch.empty(int(out_base[-1]) + 16, dtype=torch.uint8, device=device)
         L = _lib.lib()
         s = dev.stream_handle()
-        code = 1 if lay["compression"] == 1 else 8
-        _lib.check(L.ut_decode_strips(src.data_ptr(), tables[0].data_ptr(), tables[1].data_ptr(),
-                                      nstrips, code, out.data_ptr(), tables[2].data_ptr(),
-                                      tables[3].data_ptr(), status.data_ptr(), s),
-                   "ut_decode_strips")
-        _lib.check(L.ut_unpredict(out.data_ptr(), depth, h, w, ch, int(lay["predictor"]),
-                                  int(lay["bo"] == ">" and depth == 16), s), "ut_unpredict")
-        bad = int((status != 0).sum().item())
+        statuses = []
+        for code in (1, 8):
+            sel = [i for i, pl in enumerate(plans) if pl["code"] == code]
+            if not sel:
+                continue
+            cat = lambda key, base: np.concatenate(  # noqa: E731
+                [plans[i][key] + (base[i] if base is not None else 0) for i in sel])
+            tables = torch.from_numpy(np.stack([cat("offs", file_base), cat("counts", None),
+                                                cat("out_off", out_base),
+                                                cat("out_len", None)])).to(device)
+            n = tables.shape[1]
+            status = torch.empty(n, dtype=torch.int32, device=device)
+            _lib.check(L.ut_decode_strips(src.data_ptr(), tables[0].data_ptr(),
+                                          tables[1].data_ptr(), n, code, out.data_ptr(),
+                                          tables[2].data_ptr(), tables[3].data_ptr(),
+                                          status.data_ptr(), s), "ut_decode_strips")
+            statuses.append(status)
+        images = []
+        for pl, o0 in zip(plans, out_base):
+            dtype = torch.uint8 if pl["depth"] == 8 else torch.uint16
+            flat = out[int(o0):int(o0) + pl["bytes"]]
+            img = flat.view(dtype) if dtype == torch.uint8 else flat.clone().view(dtype)
+            _lib.check(L.ut_unpredict(img.data_ptr(), pl["depth"], pl["h"], pl["w"], pl["ch"],
+                                      pl["predictor"], pl["swap"], s), "ut_unpredict")
+            images.append(img.view(pl["h"], pl["w"], pl["ch"]) if pl["ch"] == 3
+                          else img.view(pl["h"], pl["w"]))
+        bad = sum(int((st != 0).sum().item()) for st in statuses)
     if bad:
-        raise DataError(f"TIFF has {bad} undecodable strip(s)")
-    return out if ch == 3 else out.view(h, w)
+        raise DataError(f"TIFF data has {bad} undecodable strip(s)")
+    return images
+
+
+def decode_tiff(data: bytes, device=None) -> torch.Tensor:
+    """Device (H, W[, 3]) uint8 / uint16 planes of one stripped TIFF."""
+    return decode_tiff_batch([data], device)[0]
 
 
 def read_image_device(path: str | Path, device=None):

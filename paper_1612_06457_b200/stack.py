@@ -243,7 +243,7 @@ def _parse_manifest_line(line: str, lineno: int, base: Path):
 def load_device_stack(manifest) -> DeviceStack:
     """The bands named by a manifest, decoded into one HBM cube (stripped TIFF
     bands decode on the device; see image_io.read_image_device)."""
-    from .image_io import read_image_device
+    from .image_io import _Unsupported, decode_tiff_batch, read_image_device
 
     manifest = Path(manifest)
     if not manifest.is_file():
@@ -256,15 +256,26 @@ def load_device_stack(manifest) -> DeviceStack:
         entries.append(_parse_manifest_line(line, lineno, manifest.parent))
     if not entries:
         raise DataError(f"manifest {manifest} lists no bands")
+    for band_id, (path, _w, _i, _f) in enumerate(entries):
+        if not path.is_file():
+            raise DataError(f"band {band_id}: image file not found: {path}")
+    # all bands in one batched device decode when every file is a stripped TIFF
+    imgs = None
+    try:
+        datas = [path.read_bytes() for path, *_ in entries]
+        imgs = decode_tiff_batch(datas)
+    except (_Unsupported, DataError, OSError):
+        imgs = None
     metas, planes = [], []
     shape, depth = None, None
     for band_id, (path, wavelength, illum, filt) in enumerate(entries):
-        if not path.is_file():
-            raise DataError(f"band {band_id}: image file not found: {path}")
-        try:
-            img, _ = read_image_device(path)
-        except DataError:
-            raise DataError(f"band {band_id}: could not decode {path}") from None
+        if imgs is not None:
+            img = imgs[band_id]
+        else:
+            try:
+                img, _ = read_image_device(path)
+            except DataError:
+                raise DataError(f"band {band_id}: could not decode {path}") from None
         if img.dim() != 2:
             raise DataError(f"band {band_id}: {path} has {img.shape[2]} channels; "
                             f"stacks are built from single-channel images")

@@ -41,13 +41,31 @@ def timed(fn):
     return out, time.perf_counter() - t0
 
 
-def gpu_arm(cfg, scene, k, depth, fmt, out_dir, reps):
+def write_bands(raw, band_dir):
+    """The page as band files + manifest, as the reference's CLI reads them
+    (deflate TIFFs written by cv2 with the reference's save_image parameters)."""
+    import cv2
+
+    band_dir.mkdir(parents=True, exist_ok=True)
+    planes = raw.planes.cpu().numpy()
+    lines = []
+    for b in range(planes.shape[0]):
+        name = f"band{b:02d}.tif"
+        cv2.imwrite(str(band_dir / name), planes[b], [cv2.IMWRITE_TIFF_COMPRESSION, 8])
+        lines.append(f"{name},{400 + 20 * b},visible")
+    (band_dir / "manifest.txt").write_text("\n".join(lines) + "\n")
+    return band_dir / "manifest.txt"
+
+
+def gpu_arm(cfg, scene, k, depth, fmt, out_dir, reps, manifest=None):
     raw = synthetic.generate(scene)
     raw = ut.DeviceStack(raw.bands, raw.planes, 16, False)
     ts = ut.TrainingSet.from_arrays(scene.xs, scene.ys, scene.labels)
     best = None
     for _ in range(reps):
         stages = {}
+        if manifest is not None:
+            raw, stages["load"] = timed(lambda: ut.load_device_stack(manifest))
         norm, stages["normalize"] = timed(lambda: ut.normalize_stack(raw))
         model, stages["fit"] = timed(lambda: ut.fit_cva(ut.assemble_matrix(norm, ts), k=k))
         res, stages["project+render"] = timed(lambda: ut.render_planes(
@@ -59,13 +77,19 @@ def gpu_arm(cfg, scene, k, depth, fmt, out_dir, reps):
     return best, len(res.plane_paths), int(np.sum(sizes)), raw
 
 
-def cpu_arm(raw, scene, k, depth, out_dir, workers):
+def cpu_arm(raw, scene, k, depth, out_dir, workers, manifest=None):
     import cv2
 
     import oracle
 
     cube = raw.planes.cpu().numpy()
     stages = {}
+    if manifest is not None:   # the reference's load_stack: cv2.imread per band
+        t0 = time.perf_counter()
+        names = [ln.split(",")[0] for ln in manifest.read_text().splitlines() if ln]
+        cube = np.stack([cv2.imread(str(manifest.parent / n), cv2.IMREAD_UNCHANGED)
+                         for n in names])
+        stages["load"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     codes, _ = oracle.normalize_stack(cube)
     stages["normalize"] = time.perf_counter() - t0
@@ -94,6 +118,8 @@ def main():
     ap.add_argument("--format", default="png")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--cpu", action="store_true")
+    ap.add_argument("--from-files", action="store_true",
+                    help="start from band TIFF files + manifest (load_stack timed)")
     ap.add_argument("--workers", type=int, default=len(os.sched_getaffinity(0)))
     args = ap.parse_args()
     w, h = (int(v) for v in args.size.lower().split("x"))
@@ -105,11 +131,15 @@ def main():
     scene = synthetic.make_scene(cfg)
     with tempfile.TemporaryDirectory() as tmp:
         out_dir = Path(tmp)
-        g, nplanes, gbytes, raw = gpu_arm(cfg, scene, k, args.depth, args.format, out_dir, args.reps)
+        manifest = None
+        if args.from_files:
+            manifest = write_bands(synthetic.generate(scene), out_dir / "bands")
+        g, nplanes, gbytes, raw = gpu_arm(cfg, scene, k, args.depth, args.format, out_dir,
+                                          args.reps, manifest)
         line = {"workload": cfg.name, "planes": nplanes, "gpu_s": {s: round(v, 4) for s, v in g.items()},
                 "gpu_png_bytes": gbytes}
         if args.cpu:
-            c, cbytes = cpu_arm(raw, scene, k, args.depth, out_dir, args.workers)
+            c, cbytes = cpu_arm(raw, scene, k, args.depth, out_dir, args.workers, manifest)
             line["cpu_s"] = {s: round(v, 4) for s, v in c.items()}
             line["cpu_png_bytes"] = cbytes
             line["cpu"] = f"oracle/ port of the reference + cv2.imwrite, workers={args.workers}"
