@@ -15,7 +15,8 @@ from .eigen import (DEFAULT_RIDGE, EigenSolution, regularize, sign_normalize,  #
 from .image_io import encode_png, encode_tiff, load_image, save_image  # noqa: F401
 from .errors import DataError, NumericError, UndertextError, UndertextWarning  # noqa: F401
 from .pipeline import (CvaPipeline, FolioStream, PcaPipeline, RenderResult,  # noqa: F401
-                       composite_filename, plane_filename, render_planes, route_points,
+                       composite_filename, fit_model, load_normalized, model_provenance,
+                       plane_filename, project_single, render_planes, route_points,
                        row_bounds)
 from .projection import (ALL_METHODS, METHOD_CVA, METHOD_LDA, METHOD_PCA,  # noqa: F401
                          METHOD_PCA_UNSUPERVISED, ProjectionModel, ScatterPair,

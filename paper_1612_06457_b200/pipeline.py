@@ -424,3 +424,62 @@ def render_planes(stack, model: ProjectionModel, specs: list[RenderSpec], out_di
         save_image(composite, path)
         result.composite_path = path
     return result
+
+
+# ------------------------------------------------- staged entry points
+# The composed stages the reference's CLI and service call (pipeline.py:56-117,
+# :193-199), on the device path.
+
+def load_normalized(manifest, crop_rect: tuple[int, int, int, int] | None = None,
+                    scope: str = "per-band"):
+    """Manifest -> loaded (device decode), optionally cropped, normalized stack
+    (pipeline.py:56-65).  Returns a DeviceStack: the cube stays in HBM for the
+    fit and projection that follow."""
+    from .stack import crop, load_device_stack, normalize_stack
+
+    stack = load_device_stack(manifest)
+    if crop_rect is not None:
+        stack = crop(stack, *crop_rect)
+    return normalize_stack(stack, scope)
+
+
+def model_provenance(stack_meta: dict, annotations_text: str | None, method: str,
+                     k: int | None, ridge: float) -> dict:
+    """The provenance dict embedded in a model file, in the reference's key
+    order (pipeline.py:68-93)."""
+    import hashlib
+
+    prov = {key: stack_meta[key] for key in ("manifest", "manifest_sha256", "crop", "scope")
+            if key in stack_meta}
+    if annotations_text is not None:
+        prov["annotations_sha256"] = hashlib.sha256(annotations_text.encode("utf-8")).hexdigest()
+    prov["method"] = method
+    prov["k"] = k if k is not None else "all"
+    prov["ridge"] = ridge
+    return prov
+
+
+def fit_model(stack, training, method: str, k: int | None = None, ridge: float = DEFAULT_RIDGE,
+              region: tuple[int, int, int, int] | None = None,
+              provenance: dict | None = None) -> ProjectionModel:
+    """Fit any method against a normalized stack (pipeline.py:96-117):
+    supervised methods sample the stack at the training points (device
+    gather), the unsupervised PCA uses every pixel of ``region``."""
+    from .annotations import assemble_matrix
+    from .projection import METHOD_PCA_UNSUPERVISED, fit
+
+    provenance = dict(provenance or {})
+    provenance.setdefault("normalized_input", stack.normalized)
+    if method == METHOD_PCA_UNSUPERVISED:
+        return fit(method, stack=stack, region=region, k=k, provenance=provenance)
+    if training is None:
+        raise DataError(f"method {method!r} needs annotations")
+    dm = assemble_matrix(stack, training)
+    return fit(method, dm=dm, k=k, ridge=ridge, provenance=provenance)
+
+
+def project_single(stack, model: ProjectionModel, k: int, workers: int = 1):
+    """One component's score plane (pipeline.py:193-199)."""
+    from .projection import project_stack
+
+    return project_stack(stack, model, components=[k], workers=workers)[0]
