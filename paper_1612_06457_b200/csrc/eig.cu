@@ -28,7 +28,10 @@ namespace {
 constexpr int N = kMaxBands;     // 32
 constexpr int LD = N + 1;        // padded row stride in shared memory
 constexpr int kThreads = N * N;  // 1024 (combine steps use all of them)
-constexpr int kTeam = 128;       // Jacobi team
+#ifndef UT_JACOBI_TEAM
+#define UT_JACOBI_TEAM 512  // measured: 128 -> 391 us, 256 -> 305, 512 -> 286, 1024 -> 301 (B = 32 PCA fit)
+#endif
+constexpr int kTeam = UT_JACOBI_TEAM;  // Jacobi team
 constexpr int kMaxC = 32;        // classes handled by the low-rank path
 
 #ifdef UT_PHASES  // dev builds: per-phase %globaltimer stamps of thread 0
