@@ -265,7 +265,8 @@ def decode_tiff_batch(datas: list, device=None) -> list:
     plans = [_tiff_plan(d) for d in datas]
     device = device or dev.require_cuda()
     file_base = np.cumsum([0] + [len(d) for d in datas])
-    out_base = np.cumsum([0] + [pl["bytes"] for pl in plans])
+    # each image starts on a 256-byte boundary (16-bit views need no copy)
+    out_base = np.cumsum([0] + [-(-pl["bytes"] // 256) * 256 for pl in plans])
     with torch.cuda.device(device):
         host = torch.empty(int(file_base[-1]), dtype=torch.uint8, pin_memory=True)
         hv = host.numpy()
@@ -296,7 +297,7 @@ def decode_tiff_batch(datas: list, device=None) -> list:
         for pl, o0 in zip(plans, out_base):
             dtype = torch.uint8 if pl["depth"] == 8 else torch.uint16
             flat = out[int(o0):int(o0) + pl["bytes"]]
-            img = flat.view(dtype) if dtype == torch.uint8 else flat.clone().view(dtype)
+            img = flat.view(dtype)
             _lib.check(L.ut_unpredict(img.data_ptr(), pl["depth"], pl["h"], pl["w"], pl["ch"],
                                       pl["predictor"], pl["swap"], s), "ut_unpredict")
             images.append(img.view(pl["h"], pl["w"], pl["ch"]) if pl["ch"] == 3
