@@ -430,6 +430,9 @@ project_tma_kernel(ProjParams p, int P, int R) {
 // per CTA, two CTAs per SM, each warp owning 32 pixels (4 MMA column groups) of
 // a 256-pixel tile (4/8-byte samples).
 constexpr int kDmmaCons = 256;
+#ifndef UT_DMMA_F2F
+#define UT_DMMA_F2F 4  // all groups on F2F: K4 7.0 -> 6.28 ms at cfg4 (ALU was the busier pipe)
+#endif
 #ifndef UT_DMMA_PROD
 #define UT_DMMA_PROD 2
 #endif
@@ -539,8 +542,12 @@ project_dmma_kernel(ProjParams p) {
           const T* row = stage + (size_t)(b < B ? b : 0) * PS + wp0 + bn;
           double x[kDmmaGroups];
 #pragma unroll
-          for (int g = 0; g < kDmmaGroups; ++g)
-            x[g] = __longlong_as_double(__double_as_longlong(widen_f64(row[8 * g])) & keep);
+          for (int g = 0; g < kDmmaGroups; ++g) {
+            // the first UT_DMMA_F2F groups widen on the conversion pipe (F2F),
+            // the rest with ALU bit operations: the two pipes share the work
+            const double w = (g < UT_DMMA_F2F) ? to_f64(row[8 * g]) : widen_f64(row[8 * g]);
+            x[g] = __longlong_as_double(__double_as_longlong(w) & keep);
+          }
 #pragma unroll
           for (int g = 0; g < kDmmaGroups; ++g) dmma_884(c0[g], c1[g], afrag[q], x[g]);
         }
