@@ -536,18 +536,18 @@ project_dmma_kernel(ProjParams p) {
       for (int q = 0; q < kMaxBands / 4; ++q) {
         if (q < nq) {  // warp-uniform
           const int b = 4 * q + bk;
-          // lanes past the last band read band 0 and zero it without a branch
-          // (a divergent select here could split the warp around the mma)
-          const long long keep = b < B ? -1LL : 0LL;
+          // lanes past the last band read band 0 (no branch: a divergent select
+          // could split the warp around the mma); their A-fragment weights are
+          // zero, so they add nothing -- a NaN / Inf there is a NaN / Inf of
+          // this pixel's band 0, which its own term propagates as well and the
+          // nonfinite guard reports
           const T* row = stage + (size_t)(b < B ? b : 0) * PS + wp0 + bn;
           double x[kDmmaGroups];
 #pragma unroll
-          for (int g = 0; g < kDmmaGroups; ++g) {
+          for (int g = 0; g < kDmmaGroups; ++g)
             // the first UT_DMMA_F2F groups widen on the conversion pipe (F2F),
-            // the rest with ALU bit operations: the two pipes share the work
-            const double w = (g < UT_DMMA_F2F) ? to_f64(row[8 * g]) : widen_f64(row[8 * g]);
-            x[g] = __longlong_as_double(__double_as_longlong(w) & keep);
-          }
+            // the rest with ALU bit operations
+            x[g] = (g < UT_DMMA_F2F) ? to_f64(row[8 * g]) : widen_f64(row[8 * g]);
 #pragma unroll
           for (int g = 0; g < kDmmaGroups; ++g) dmma_884(c0[g], c1[g], afrag[q], x[g]);
         }
