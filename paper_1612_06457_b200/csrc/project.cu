@@ -842,6 +842,151 @@ stretch_kernel(const float* __restrict__ scores, const float* __restrict__ minma
   }
 }
 
+// K5 on a bulk-copy ring: the fp32 score planes stream through shared memory
+// (cp.async.bulk, 4 x 16 KB stages, one producer warp) so the loads in flight
+// do not cost registers; 8 consumer warps turn 16 scores each per tile into
+// codes with the same arithmetic as stretch_kernel (fp32 fast path, fp64 redo
+// near ties, bit-exact) and store them straight to global memory.
+constexpr int kK5P = 4096;        // scores per tile (16 KB)
+constexpr int kK5Stages = 4;
+constexpr int kK5Cons = 256;      // consumer threads, 16 scores each
+
+template <int DEPTH>
+struct StretchPlane {
+  using Code = typename std::conditional<DEPTH == 8, uint8_t, uint16_t>::type;
+  static constexpr double top = DEPTH == 8 ? 255.0 : 65535.0;
+  double lo, sc;
+  float lof, scf;
+  bool flat;
+  __device__ __forceinline__ Code exact(float v) const {
+    double x = ((double)v - lo) * sc;
+    x = fmin(fmax(x, 0.0), top);
+    return (Code)(int)floor(x + 0.5);
+  }
+  __device__ __forceinline__ void codes16(const float* v, Code* out) const {
+    if (flat) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) out[i] = (Code)0;
+      return;
+    }
+    if constexpr (DEPTH == 8) {
+      bool tie = false;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float x = (v[i] - lof) * scf;
+        tie |= fabsf(x - rintf(x)) >= 0.5f - 2e-4f;
+        unsigned short u;
+        asm("cvt.rni.sat.u8.f32 %0, %1;" : "=h"(u) : "f"(x));
+        out[i] = (Code)u;
+      }
+      if (!tie) return;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) out[i] = exact(v[i]);
+  }
+};
+
+template <int DEPTH>
+__global__ void __launch_bounds__(kK5Cons + 32, 2)
+stretch_tma_kernel(const float* __restrict__ scores, const float* __restrict__ minmax, int k,
+                   int ld_mm, int64_t npix, void* __restrict__ codes_raw) {
+  using SP = StretchPlane<DEPTH>;
+  using Code = typename SP::Code;
+  extern __shared__ __align__(128) unsigned char k5dyn[];
+  float* stages = reinterpret_cast<float*>(k5dyn);
+  uint64_t* full = reinterpret_cast<uint64_t*>(k5dyn + (size_t)kK5Stages * kK5P * sizeof(float));
+  uint64_t* empty = full + kK5Stages;
+  __shared__ SP planes[kMaxBands];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int c = tid; c < k; c += blockDim.x) {
+    SP q;
+    const double lo = -(double)minmax[c], hi = (double)minmax[ld_mm + c];
+    q.lo = lo;
+    q.flat = (lo == hi) || !(lo < hi);  // constant plane (rendering.py:128-129)
+    q.sc = q.flat ? 0.0 : SP::top / (hi - lo);
+    q.lof = (float)lo;
+    q.scf = (float)q.sc;
+    planes[c] = q;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kK5Stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kK5Cons / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t tpp = (npix + kK5P - 1) / kK5P;   // tiles per plane
+  const int64_t ntiles = tpp * k;
+  if (warp == kK5Cons / 32) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int i = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int st = i % kK5Stages;
+        if (i >= kK5Stages) mbar_wait(&empty[st], ((i / kK5Stages) - 1) & 1);
+        const int64_t c = t / tpp, off = (t - c * tpp) * kK5P;
+        const int64_t n = (npix - off) < kK5P ? (npix - off) : kK5P;
+        const uint32_t bytes = (uint32_t)(n * sizeof(float));
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(stages + (size_t)st * kK5P, scores + c * npix + off, bytes, &full[st], pol);
+      }
+    }
+  } else {
+    Code* codes = static_cast<Code*>(codes_raw);
+    int i = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int st = i % kK5Stages;
+      mbar_wait(&full[st], (i / kK5Stages) & 1);
+      const int64_t c = t / tpp, off = (t - c * tpp) * kK5P;
+      const int64_t n = (npix - off) < kK5P ? (npix - off) : kK5P;
+      const int lp = tid * 16;
+      if (lp + 16 <= n) {
+        const float* src = stages + (size_t)st * kK5P + lp;
+        float v[16];
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) *reinterpret_cast<float4*>(v + q) = *reinterpret_cast<const float4*>(src + q);
+        Code out[16];
+        planes[c].codes16(v, out);
+        Code* o = codes + c * npix + off + lp;
+        st_stream_u4(o, *reinterpret_cast<const uint4*>(out));
+        if constexpr (DEPTH == 16) st_stream_u4(o + 8, *reinterpret_cast<const uint4*>(out + 8));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+}
+
+constexpr size_t kK5Smem = (size_t)kK5Stages * kK5P * sizeof(float) + 2 * kK5Stages * sizeof(uint64_t);
+
+template <int DEPTH>
+int launch_stretch_tma(const float* scores, const float* minmax, int k, int ld_mm, int64_t npix,
+                       void* codes, cudaStream_t st) {
+  auto kern = stretch_tma_kernel<DEPTH>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK5Smem);
+    if (e != cudaSuccess) return cuda_status(e, "stretch_tma smem attribute");
+    attr = true;
+  }
+  const int64_t ntiles = ((npix + kK5P - 1) / kK5P) * k;
+  int64_t grid = 2 * (int64_t)sm_count();
+  if (grid > ntiles) grid = ntiles;
+  kern<<<(unsigned)grid, kK5Cons + 32, kK5Smem, st>>>(scores, minmax, k, ld_mm, npix, codes);
+  UT_CHECK_LAUNCH("stretch_tma_kernel");
+  return UT_OK;
+}
+
+bool k5_tma_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("UT_K5_TMA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 }  // namespace
 }  // namespace ut
 
@@ -909,6 +1054,9 @@ int ut_stretch(const float* scores, const float* minmax, int32_t k, int32_t ld_m
   cudaStream_t st = as_stream(stream);
   const bool vec16 = (npix % 16 == 0) && (reinterpret_cast<uintptr_t>(scores) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(codes) % 16 == 0);
+  if (vec16 && k5_tma_enabled())
+    return depth == 8 ? launch_stretch_tma<8>(scores, minmax, k, ld_minmax, npix, codes, st)
+                      : launch_stretch_tma<16>(scores, minmax, k, ld_minmax, npix, codes, st);
   dim3 grid;
   if (vec16) {
     const int64_t chunks = npix / 16;
