@@ -847,9 +847,14 @@ stretch_kernel(const float* __restrict__ scores, const float* __restrict__ minma
 // do not cost registers; 8 consumer warps turn 16 scores each per tile into
 // codes with the same arithmetic as stretch_kernel (fp32 fast path, fp64 redo
 // near ties, bit-exact) and store them straight to global memory.
-constexpr int kK5P = 4096;        // scores per tile (16 KB)
-constexpr int kK5Stages = 4;
-constexpr int kK5Cons = 256;      // consumer threads, 16 scores each
+#ifndef UT_K5_P
+#define UT_K5_P 8192      // measured (cfg4, 5 planes): 4096 x 4: 1.11 ms, x 6: 1.08, 8192 x 2: 1.09, 8192 x 3: 1.01
+#define UT_K5_STAGES 3
+#endif
+constexpr int kK5P = UT_K5_P;            // scores per tile (32 KB)
+constexpr int kK5Stages = UT_K5_STAGES;
+constexpr int kK5Cons = 256;      // consumer threads, 16 scores each per pass
+static_assert(kK5P % (kK5Cons * 16) == 0, "a tile is whole consumer passes");
 
 template <int DEPTH>
 struct StretchPlane {
@@ -940,17 +945,21 @@ stretch_tma_kernel(const float* __restrict__ scores, const float* __restrict__ m
       mbar_wait(&full[st], (i / kK5Stages) & 1);
       const int64_t c = t / tpp, off = (t - c * tpp) * kK5P;
       const int64_t n = (npix - off) < kK5P ? (npix - off) : kK5P;
-      const int lp = tid * 16;
-      if (lp + 16 <= n) {
-        const float* src = stages + (size_t)st * kK5P + lp;
-        float v[16];
 #pragma unroll
-        for (int q = 0; q < 16; q += 4) *reinterpret_cast<float4*>(v + q) = *reinterpret_cast<const float4*>(src + q);
-        Code out[16];
-        planes[c].codes16(v, out);
-        Code* o = codes + c * npix + off + lp;
-        st_stream_u4(o, *reinterpret_cast<const uint4*>(out));
-        if constexpr (DEPTH == 16) st_stream_u4(o + 8, *reinterpret_cast<const uint4*>(out + 8));
+      for (int r = 0; r < kK5P / (kK5Cons * 16); ++r) {
+        const int lp = (r * kK5Cons + tid) * 16;
+        if (lp + 16 <= n) {
+          const float* src = stages + (size_t)st * kK5P + lp;
+          float v[16];
+#pragma unroll
+          for (int q = 0; q < 16; q += 4)
+            *reinterpret_cast<float4*>(v + q) = *reinterpret_cast<const float4*>(src + q);
+          Code out[16];
+          planes[c].codes16(v, out);
+          Code* o = codes + c * npix + off + lp;
+          st_stream_u4(o, *reinterpret_cast<const uint4*>(out));
+          if constexpr (DEPTH == 16) st_stream_u4(o + 8, *reinterpret_cast<const uint4*>(out + 8));
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
