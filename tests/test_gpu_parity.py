@@ -577,3 +577,30 @@ def test_device_stack_api_paths():
     assert m2.method == "pca_unsupervised" and m2.coefficients.shape == (cfg.bands, 2)
     with pytest.raises(ut.DataError):
         ut.fit("nope", dm=dm)
+
+
+@pytest.mark.parametrize("k,npix", [(3, 8192 * 2 + 48), (1, 16), (32, 8192 + 4096 + 16), (5, 3 * 8192)])
+def test_stretch_ring_multiplane_tails(k, npix):
+    """K5's bulk-copy ring over several planes with partial last tiles (32 KB
+    tiles of 8192 scores), 8- and 16-bit codes, against the oracle."""
+    from paper_1612_06457_b200.rendering import stretch_planes
+
+    rng = np.random.default_rng(k * 1000 + npix % 977)
+    planes = rng.normal(0, 3, size=(k, npix)).astype(np.float32)
+    planes[0, ::5] = 1.25                                  # repeated values / ties
+    lo = planes.min(axis=1).astype(np.float32)
+    hi = planes.max(axis=1).astype(np.float32)
+    if k > 1:
+        planes[1] = 4.0                                    # a constant plane -> zeros
+        lo[1] = hi[1] = 4.0
+    scores = torch.from_numpy(planes.reshape(k, 1, npix)).cuda()
+    mm = torch.from_numpy(np.concatenate([-lo, hi]).astype(np.float32)).cuda()
+    for depth in (8, 16):
+        got = stretch_planes(scores, mm, depth=depth).cpu().numpy().reshape(k, npix)
+        for c in range(k):
+            if lo[c] == hi[c]:
+                assert not got[c].any()
+                continue
+            want = oracle.linear_to_codes(planes[c].astype(np.float64), float(lo[c]), float(hi[c]),
+                                          depth)
+            assert np.array_equal(got[c], want), (c, depth)
