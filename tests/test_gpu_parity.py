@@ -604,3 +604,40 @@ def test_stretch_ring_multiplane_tails(k, npix):
             want = oracle.linear_to_codes(planes[c].astype(np.float64), float(lo[c]), float(hi[c]),
                                           depth)
             assert np.array_equal(got[c], want), (c, depth)
+
+
+@pytest.mark.parametrize("bands,k", [(23, 5), (5, 4), (32, 8), (17, 6)])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_dmma_projector_padded_bands(bands, k, dtype):
+    """The fp64 tensor-core projector (K >= 4, 4/8-byte samples) with band counts
+    that are not multiples of 4: the padded lanes read band 0 and must add
+    nothing (zero weights); awkward values (zeros, -0, subnormal, large)."""
+    rng = np.random.default_rng(bands * 10 + k)
+    cube = (rng.normal(size=(bands, 29, 64)) * 50).astype(dtype)
+    cube[:, 0, :7] = 0
+    cube[:, 1, :5] = -0.0
+    cube[0, 2, :3] = np.finfo(dtype).tiny / 4           # subnormal
+    cube[1 % bands, 3, :2] = 1e6
+    coef = rng.normal(size=(bands, k))
+    mean = rng.normal(size=bands)
+    model = ut.ProjectionModel("cva", mean, None, coef, np.ones(k))
+    ds = ut.DeviceStack(ut.stack.default_bands(bands), torch.from_numpy(cube).cuda(), 8, True)
+    planes = [p.values.double().cpu().numpy() for p in ut.project_stack(ds, model, precision="fp64")]
+    ref = oracle.project(cube, {"mean": mean, "std": None, "coefficients": coef})
+    for got, want in zip(planes, ref):
+        rng_ = float(want.max() - want.min())
+        assert float(np.abs(got - want).max()) <= 1e-7 * rng_
+
+
+@pytest.mark.parametrize("bands", [23, 32])
+def test_dmma_projector_nonfinite_band0(bands):
+    """A NaN / Inf in band 0 (the band the padded lanes read) is reported."""
+    rng = np.random.default_rng(5)
+    coef = rng.normal(size=(bands, 5))
+    model = ut.ProjectionModel("cva", np.zeros(bands), None, coef, np.ones(5))
+    for bad in (np.nan, np.inf):
+        cube = rng.normal(size=(bands, 16, 64)).astype(np.float32)
+        cube[0, 7, 9] = bad
+        ds = ut.DeviceStack(ut.stack.default_bands(bands), torch.from_numpy(cube).cuda(), 8, True)
+        with pytest.raises(ut.DataError, match="NaN or Inf"):
+            ut.project_stack(ds, model, precision="fp64")
