@@ -24,7 +24,10 @@ namespace {
 constexpr int kChunk = 128;      // points staged per step
 constexpr int kThreads = 256;
 constexpr int kMaxG = 1024;      // point ranges (CTAs)
-constexpr int kMinPerCta = 128;  // one staged chunk per CTA when n <= 128 * 1024
+#ifndef UT_K1_MINPER
+#define UT_K1_MINPER 256  // two pipelined chunks per CTA, one wave at cfg 4 (60k points): 140 -> 123 us
+#endif
+constexpr int kMinPerCta = UT_K1_MINPER;  // points per CTA at least (multiple of kChunk)
 constexpr int kMaxClasses = 16;  // per launch; more classes -> several launches
 constexpr int kRows = kMaxBands + 1;                    // bands + ones row
 constexpr int kMaxEnt = kRows * (kRows + 1) / 2;        // 561
