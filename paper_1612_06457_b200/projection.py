@@ -169,6 +169,10 @@ class CvaDevice:
         self.mlen = int(_lib.lib().ut_moment_len(bands))
         b, c = bands, classes
         self.moments = torch.zeros(groups * c * self.mlen, dtype=torch.float64, device=device)
+        # sharded fits: this rank's record lives in its own buffer; as a slice of
+        # `moments` it would overlap the all_gather output of rank 0's slot
+        self._local = self.moments[: c * self.mlen] if groups == 1 else \
+            torch.zeros(c * self.mlen, dtype=torch.float64, device=device)
         sizes = dict(within=b * b, between=b * b, class_means=c * b, counts=c, grand_mean=b,
                      evals=b, evecs=b * b, aux=b)
         total = sum(sizes.values())
@@ -181,7 +185,7 @@ class CvaDevice:
         self.out = _lib.CvaOut(*(self.views[n].data_ptr() for n in sizes), self.info.data_ptr())
 
     def local_moments(self) -> torch.Tensor:
-        return self.moments[: self.c * self.mlen]
+        return self._local
 
     def moments_from(self, values: torch.Tensor, ld: int, cls_d: torch.Tensor, n: int):
         L = _lib.lib()
@@ -191,7 +195,7 @@ class CvaDevice:
         need = L.ut_class_moments_ws(n, self.b, self.c)
         ws = dev.workspace("class_moments", need, values.device)
         _lib.check(L.ut_class_moments(values.data_ptr(), ld, cls_d.data_ptr(), n, self.b, self.c,
-                                      None, self.moments.data_ptr(), ws.data_ptr(), ws.numel(),
+                                      None, self._local.data_ptr(), ws.data_ptr(), ws.numel(),
                                       dev.stream_handle()), "ut_class_moments")
 
     def moments_from_cube(self, cube, xy_d: torch.Tensor, cls_d: torch.Tensor, n: int,
@@ -205,7 +209,7 @@ class CvaDevice:
                            xy_d.device)
         _lib.check(L.ut_cube_class_moments(C.byref(cube), xy_d.data_ptr(), cls_d.data_ptr(), n,
                                            self.c, None if pivots is None else pivots.data_ptr(),
-                                           self.moments.data_ptr(), first_bad.data_ptr(),
+                                           self._local.data_ptr(), first_bad.data_ptr(),
                                            ws.data_ptr(), ws.numel(), dev.stream_handle()),
                    "ut_cube_class_moments")
 
@@ -299,6 +303,8 @@ class PcaDevice:
         self.mlen = int(_lib.lib().ut_moment_len(bands))
         b = bands
         self.moments = torch.zeros(groups * self.mlen, dtype=torch.float64, device=device)
+        self._local = self.moments[: self.mlen] if groups == 1 else \
+            torch.zeros(self.mlen, dtype=torch.float64, device=device)  # see CvaDevice
         sizes = dict(mean=b, std=b, corr=b * b, evals=b, evecs=b * b)
         self.flat = torch.zeros(sum(sizes.values()), dtype=torch.float64, device=device)
         self.views, off = {}, 0
@@ -309,12 +315,12 @@ class PcaDevice:
         self.out = _lib.PcaOut(*(self.views[n].data_ptr() for n in sizes), self.info.data_ptr())
 
     def local_moments(self) -> torch.Tensor:
-        return self.moments[: self.mlen]
+        return self._local
 
     def moments_from(self, cube, x0, y0, w, h, device):
         L = _lib.lib()
         ws = dev.workspace("region_moments", L.ut_region_moments_ws(self.b), device)
-        _lib.check(L.ut_region_moments(C.byref(cube), x0, y0, w, h, self.moments.data_ptr(),
+        _lib.check(L.ut_region_moments(C.byref(cube), x0, y0, w, h, self._local.data_ptr(),
                                        ws.data_ptr(), ws.numel(), dev.stream_handle()),
                    "ut_region_moments")
 

@@ -118,3 +118,18 @@ def test_product_never_imports_oracle():
     for src in pkg.rglob("*.py"):
         text = src.read_text()
         assert "import oracle" not in text and "from oracle" not in text, src
+
+
+def test_sharded_local_record_does_not_alias_gather_output():
+    """all_gather_into_tensor(moments, local): with NCCL an input that overlaps
+    another rank's output slot is a race, so a sharded fit keeps its own record
+    in a separate buffer (an unsharded fit writes slot 0 directly)."""
+    from paper_1612_06457_b200.projection import CvaDevice, PcaDevice
+
+    for fit in (CvaDevice(8, 3, "cpu", groups=4), PcaDevice(8, "cpu", groups=4)):
+        loc, out = fit.local_moments(), fit.moments
+        assert loc.numel() * 4 == out.numel()
+        lo, hi = loc.data_ptr(), loc.data_ptr() + loc.numel() * 8
+        assert hi <= out.data_ptr() or lo >= out.data_ptr() + out.numel() * 8
+    for fit in (CvaDevice(8, 3, "cpu"), PcaDevice(8, "cpu")):
+        assert fit.local_moments().data_ptr() == fit.moments.data_ptr()
