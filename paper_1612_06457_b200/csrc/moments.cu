@@ -28,6 +28,10 @@ constexpr int kMaxG = 1024;      // point ranges (CTAs)
 #define UT_K1_MINPER 256  // two pipelined chunks per CTA, one wave at cfg 4 (60k points): 140 -> 123 us
 #endif
 constexpr int kMinPerCta = UT_K1_MINPER;  // points per CTA at least (multiple of kChunk)
+#ifndef UT_K1_SMALL_G
+#define UT_K1_SMALL_G 296
+#endif
+constexpr int kSmallG = UT_K1_SMALL_G;  // up to this many 128-point CTAs, no 2-chunk minimum
 constexpr int kMaxClasses = 16;  // per launch; more classes -> several launches
 constexpr int kRows = kMaxBands + 1;                    // bands + ones row
 constexpr int kMaxEnt = kRows * (kRows + 1) / 2;        // 561
@@ -350,7 +354,12 @@ Layout make_layout(int64_t n, int b, int c) {
   L.n = n;
   L.bands = b;
   L.classes = c;
-  int64_t G = (n + kMinPerCta - 1) / kMinPerCta;
+  // Small point sets (a row shard's share at 4-8 GPUs): one 128-point chunk
+  // per CTA, more CTAs in flight for the latency-bound gather (cfg 4 at 8
+  // shards, 4590 points: 75 -> 63 us).  Larger sets keep two pipelined chunks
+  // per CTA so they run in one wave.  G stays a function of n only.
+  int64_t G = (n + kChunk - 1) / kChunk;
+  if (G > kSmallG) G = (n + kMinPerCta - 1) / kMinPerCta;
   if (G > kMaxG) G = kMaxG;
   if (G < 1) G = 1;
   int64_t span = (n + G - 1) / G;
