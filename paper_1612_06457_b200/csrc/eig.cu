@@ -493,14 +493,15 @@ __device__ bool cva_low_rank_gj(Smem& s, int n, int C, double ridge, int want,
       __syncthreads();
       return false;
     }
-    const double inv = __drcp_rn(piv);
-    const int w = wl - (k + 1);  // columns > k
-    for (int e = tid; e < n * w; e += nt) {
-      const int i = e / w, q = k + 1 + (e - i * w);
-      if (i == k) continue;
-      const double g = s.m[i * LD + k] * inv;
-      if (q < n) s.m[i * LD + q] -= g * s.m[k * LD + q];
-      else s.h[i * LD + (q - n)] -= g * s.h[k * LD + (q - n)];
+    // warp i owns row i (n <= 32 rows, 32 warps): the factor is warp-uniform
+    // and the lanes walk the columns > k with no index division
+    const int i = tid >> 5;
+    if (i < n && i != k) {
+      const double g = s.m[i * LD + k] * __drcp_rn(piv);
+      for (int q = k + 1 + (tid & 31); q < wl; q += 32) {
+        if (q < n) s.m[i * LD + q] -= g * s.m[k * LD + q];
+        else s.h[i * LD + (q - n)] -= g * s.h[k * LD + (q - n)];
+      }
     }
     __syncthreads();
   }

@@ -200,20 +200,6 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restri
   const int E = ent_count(B);
   const int64_t j0 = (int64_t)blockIdx.x * L.span;
   const int64_t j1 = j0 + L.span < L.n ? j0 + L.span : L.n;
-  for (int i = tid; i < R; i += blockDim.x) {
-    const int base = i * R - i * (i - 1) / 2;
-    for (int j = i; j < R; ++j) {
-      s.pi[base + j - i] = (unsigned char)i;
-      s.pj[base + j - i] = (unsigned char)j;
-    }
-  }
-  for (int e = tid; e < C * E; e += blockDim.x) s.acc[e] = 0.0;
-  for (int e = tid; e < C * B; e += blockDim.x) {
-    const int c = e / B, b = e - c * B;
-    const int pj = pivots[c];
-    s.pivot[e] = (pj >= 0 && src.valid(pj)) ? src.at_global(b, pj) : 0.0;
-  }
-  __syncthreads();
   // Staging: thread -> point p = tid % 128, bands tid/128, +2, +4, ...  The
   // gather is random-access and latency-bound, so it is software-pipelined:
   // coordinates / labels are loaded two chunks ahead and raw samples one chunk
@@ -248,11 +234,27 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restri
       nv[u] = (nl >= 0 && b < B) ? src.raw(b, ncc) : typename Src::Raw(0);
     }
   };
+  // the first chunk's gather is issued before the set-up below (pivot
+  // loads, tables) so their latencies overlap
   if (j0 < j1) {
     load_coord(j0);
     load_samples(j0);
     if (j0 + kChunk < j1) load_coord(j0 + kChunk);
   }
+  for (int i = tid; i < R; i += blockDim.x) {
+    const int base = i * R - i * (i - 1) / 2;
+    for (int j = i; j < R; ++j) {
+      s.pi[base + j - i] = (unsigned char)i;
+      s.pj[base + j - i] = (unsigned char)j;
+    }
+  }
+  for (int e = tid; e < C * E; e += blockDim.x) s.acc[e] = 0.0;
+  for (int e = tid; e < C * B; e += blockDim.x) {
+    const int c = e / B, b = e - c * B;
+    const int pj = pivots[c];
+    s.pivot[e] = (pj >= 0 && src.valid(pj)) ? src.at_global(b, pj) : 0.0;
+  }
+  __syncthreads();
   for (int64_t q0 = j0; q0 < j1; q0 += kChunk) {
     const int count = (int)((j1 - q0) < kChunk ? (j1 - q0) : kChunk);
     if (tid == 0) *s.mask_p = 0u;
