@@ -641,3 +641,21 @@ def test_dmma_projector_nonfinite_band0(bands):
         ds = ut.DeviceStack(ut.stack.default_bands(bands), torch.from_numpy(cube).cuda(), 8, True)
         with pytest.raises(ut.DataError, match="NaN or Inf"):
             ut.project_stack(ds, model, precision="fp64")
+
+
+@pytest.mark.parametrize("n", [37887, 37888, 37889, 75776, 75777])
+def test_class_moments_partition_boundaries(n):
+    """K1 splits n points into one 128-point chunk per CTA up to 296 CTAs and
+    two-chunk CTAs above (moments.cu make_layout); both regimes, the exact
+    boundary and ragged last ranges match the oracle's two-pass scatter."""
+    rng = np.random.default_rng(n)
+    b = 32
+    values = 0.5 + 0.05 * rng.standard_normal((b, n))
+    labels = rng.integers(0, 6, n)
+    values[:, labels == 3] += 0.1  # distinct class means
+    sp = ut.compute_scatter(dm_of(values, labels))
+    want = oracle.scatter(values, labels)
+    assert np.array_equal(sp.counts, want["counts"])
+    for got, key in ((sp.within, "within"), (sp.between, "between"),
+                     (sp.class_means, "class_means"), (sp.grand_mean, "grand_mean")):
+        assert rel_close(got, want[key], 1e-9), key
