@@ -188,22 +188,22 @@ def host_cube(stack):
     return host
 
 
-def cpu_reference(cube_np, scene, cfg, rows, workers, threads_note):
+def cpu_reference(sample, train_values, scene, cfg, workers):
     """One bounded sample of the workload through the oracle port of the
-    reference: assemble + fit_cva on the full training set, then project +
-    rescale_full of `rows` image rows.  Returns (seconds, pixels)."""
+    reference: fit_cva on the full training matrix (B x N, already gathered),
+    then project + rescale_full of the ``sample`` rows (B, rows, W).  PCA fits
+    on the sample rows (its covariance is a per-pixel pass).  Returns
+    (seconds, pixels)."""
     import oracle
 
     t0 = time.perf_counter()
     if cfg.method == "cva":
-        values = oracle.assemble(cube_np, scene.xs, scene.ys)
-        model = oracle.fit_cva(values, scene.labels, k=cfg.k)
-    else:  # PCA: the covariance pass is per pixel too -> fit on the sampled rows
-        model = oracle.fit_pca_unsupervised(cube_np[:, :max(rows, 2)], k=cfg.k)
-    sample = cube_np[:, :rows]
+        model = oracle.fit_cva(train_values, scene.labels, k=cfg.k)
+    else:
+        model = oracle.fit_pca_unsupervised(sample, k=cfg.k)
     scores = oracle.project(sample, model, workers=workers)
     _ = [oracle.rescale_full(s) for s in scores]
-    return time.perf_counter() - t0, rows * cfg.width
+    return time.perf_counter() - t0, sample.shape[1] * sample.shape[2]
 
 
 def cpu_threads():
@@ -217,62 +217,97 @@ def cpu_threads():
     return n, blas
 
 
-def pick_rows(cube_np, scene, cfg, workers, seconds):
-    """Rows so that one sample takes about `seconds` of CPU time."""
-    probe = max(16, min(cfg.height, 256))
-    t, px = cpu_reference(cube_np, scene, cfg, probe, workers, None)
-    t_fit, _ = cpu_reference(cube_np, scene, cfg, 1, workers, None)
-    per_row = max((t - t_fit) / probe, 1e-6)
-    rows = int(max(16, min(cfg.height, (seconds - t_fit) / per_row)))
-    return rows
+def pick_rows(probe_sample, train_values, scene, cfg, workers, seconds):
+    """Rows so that one sample step takes about ``seconds`` of CPU time."""
+    t, px = cpu_reference(probe_sample, train_values, scene, cfg, workers)
+    t_fit, _ = cpu_reference(probe_sample[:, :2], train_values, scene, cfg, workers)
+    per_row = max((t - t_fit) / probe_sample.shape[1], 1e-6)
+    return int(max(16, min(cfg.height, (seconds - t_fit) / per_row)))
+
+
+def bench_config(cfg, world, args, n_train):
+    """The ``config`` object of the JSON line -- identical for both arms."""
+    cube_bytes = cfg.pixels * cfg.bands * cfg.sample_bytes // max(world, 1)
+    use_graph = world == 1 and cfg.pixels <= (1 << 24) and not args.no_graph
+    return {"workload": cfg.name, "height": cfg.height, "width": cfg.width,
+            "bands": cfg.bands, "sample": str(cfg.dtype).replace("torch.", ""),
+            "classes": cfg.classes, "training_px": int(n_train), "components": cfg.k,
+            "parallelism": f"rows{world}",
+            "l2": "inputs > L2 (cube %.1f GB per GPU)" % (cube_bytes / 1e9)
+                  if cube_bytes > 126e6 else
+                  "cube fits L2 (%.1f MB); no flush: a repeated step re-reads the same "
+                  "cube, as a resident-data service would" % (cube_bytes / 1e6),
+            "cuda_graph": use_graph}
+
+
+def repo_libs_mapped():
+    """In-tree shared objects mapped into this process (the reference arm must
+    map none)."""
+    try:
+        maps = Path("/proc/self/maps").read_text()
+    except OSError:
+        return []
+    return sorted({ln.split()[-1] for ln in maps.splitlines()
+                   if str(ROOT) in ln and ln.rstrip().endswith(".so")})
 
 
 # ------------------------------------------------------------------ arms
 
 def run_reference(args):
-    """--impl reference: the reference algorithm (numpy port in oracle/, the
-    reference itself is Python and cannot travel) on this box's host cores."""
+    """--impl reference: the reference algorithm (the numpy port in oracle/; the
+    reference itself is Python and cannot travel to the box) on this box's
+    host cores.  Inputs come from oracle/synth.py, the host restatement of the
+    device generator (bit-identical samples), so this arm never maps the
+    repo's CUDA library or touches the GPU."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import torch
-
+    from oracle import synth as host_synth
     from paper_1612_06457_b200 import synthetic
 
     cfg = cfg_of(args)
     scene = synthetic.make_scene(cfg)
-    torch.cuda.set_device(0)
-    stack = synthetic.generate(scene)      # data generation only (setup)
-    cube_np = host_cube(stack).numpy()
-    del stack
-    torch.cuda.empty_cache()
     cores, blas = cpu_threads()
+    t_gen = time.perf_counter()
+    train = host_synth.pixels(scene, scene.ys, scene.xs).astype(np.float64) \
+        if cfg.method == "cva" else None
+    probe = host_synth.rows(scene, 0, min(cfg.height, 64), procs=cores)
     steps = args.steps + args.warmup
-    rows = pick_rows(cube_np, scene, cfg, cores, args.ref_budget / max(steps, 1))
+    rows = pick_rows(probe, train, scene, cfg, cores, args.ref_budget / max(steps, 1))
+    r0 = (cfg.height - rows) // 2            # a block from the middle of the image
+    sample = host_synth.rows(scene, r0, r0 + rows, procs=cores)
+    t_gen = time.perf_counter() - t_gen
     times = []
     for i in range(steps):
-        t, px = cpu_reference(cube_np, scene, cfg, rows, cores, None)
+        t, px = cpu_reference(sample, train, scene, cfg, cores)
         if i >= args.warmup:
             times.append(t)
     sec = float(np.mean(times))
     value = px / sec / 1e6
-    sample = (f"fit on all {len(scene.xs)} training px + project/stretch of {rows} of "
-              f"{cfg.height} rows ({px} px) per step; numpy port of the reference "
-              f"(oracle/cva_pca.py), workers={cores}, BLAS threads={blas}")
+    libs = repo_libs_mapped()
+    if libs:
+        raise RuntimeError(f"reference arm mapped repo libraries: {libs}")
+    fit = (f"fit_cva on all {len(scene.xs)} training px (gathered during setup)"
+           if cfg.method == "cva" else f"PCA fit on the {rows} sampled rows")
+    sample_txt = (f"{fit} + project/stretch of rows {r0}..{r0 + rows} of {cfg.height} "
+                  f"({px} px) per step; numpy port of the reference (oracle/cva_pca.py), "
+                  f"workers={cores}, BLAS threads={blas}; inputs from oracle/synth.py "
+                  f"(host restatement of the device generator, {t_gen:.1f} s setup)")
     line = {
         "metric": "CVA Mpixel/s (scatter+eigen+projection)" if cfg.method == "cva"
         else "PCA Mpixel/s (covariance+eigen+projection)",
         "value": round(value, 3), "unit": "Mpixel/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "bands": cfg.bands, "classes": cfg.classes,
-                   "components": cfg.k, "pixels": cfg.pixels},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE.json generator, host restatement; seed %d)" % cfg.seed,
+        "config": bench_config(cfg, world, args, len(scene.xs)),
         "cpu_baseline": {"value": round(value, 3), "unit": "Mpixel/s", "cores": cores,
-                         "kind": "port", "sample": sample},
+                         "kind": "port", "sample": sample_txt},
         "e2e": {"value": round(value, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "repo_libs_mapped": libs,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -567,8 +602,13 @@ def run_b200(args):
             host = host_cube(stack)
         cube_np = host.numpy()
         cores, blas = cpu_threads()
-        rows = pick_rows(cube_np, scene, cfg, cores, args.cpu_seconds)
-        t, px = cpu_reference(cube_np, scene, cfg, rows, cores, None)
+        train = None
+        if cfg.method == "cva":
+            import oracle
+
+            train = oracle.assemble(cube_np, scene.xs, scene.ys)
+        rows = pick_rows(cube_np[:, :64], train, scene, cfg, cores, args.cpu_seconds)
+        t, px = cpu_reference(cube_np[:, :rows], train, scene, cfg, cores)
         cpu = {"value": round(px / t / 1e6, 3), "unit": "Mpixel/s", "cores": cores,
                "kind": "port",
                "sample": (f"fit on all {len(scene.xs)} training px + project/stretch of "
@@ -586,17 +626,7 @@ def run_b200(args):
             "vs_baseline": None,
             "dtype": "f64" if pipe_precision(args) == "fp64" else "f32 (fit f64)",
             "data": "synthetic (BASELINE.json generator, generated in HBM; seed %d)" % cfg.seed,
-            "config": {"workload": cfg.name, "height": cfg.height, "width": cfg.width,
-                       "bands": cfg.bands, "sample": str(cfg.dtype).replace("torch.", ""),
-                       "classes": cfg.classes, "training_px": int(len(scene.xs)),
-                       "components": cfg.k, "parallelism": f"rows{world}",
-                       "l2": "inputs > L2 (cube %.1f GB per GPU)" %
-                             (stack.planes.numel() * stack.planes.element_size() / 1e9)
-                             if stack.planes.numel() * stack.planes.element_size() > 126e6
-                             else "cube fits L2 (%.1f MB); no flush: a repeated step re-reads "
-                                  "the same cube, as a resident-data service would" %
-                                  (stack.planes.numel() * stack.planes.element_size() / 1e6),
-                       "cuda_graph": use_graph},
+            "config": bench_config(cfg, world, args, len(scene.xs)),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "kernel": "project_kernel (K4)",

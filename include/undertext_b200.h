@@ -111,6 +111,13 @@ int ut_class_moments(const double* values, int64_t ld, const int32_t* cls,
                      int64_t n, int32_t bands, int32_t classes, const int32_t* pivots,
                      double* moments, void* ws, size_t ws_bytes, void* stream);
 
+/* standardize(dm) (projection.py:152-169): out[b, j] = (x[b, j] - mean_b) / std_b
+ * with the N - 1 divisor and std = 1 for a constant row; n >= 2 (DataError
+ * otherwise).  values / out: B x n fp64, row strides ld / ld_out (elements);
+ * may alias when ld == ld_out.  Feeds fit_lda (projection.py:240-260). */
+int ut_standardize(const double* values, int64_t ld, int32_t bands, int64_t n, double* out,
+                   int64_t ld_out, double* mean, double* std, void* stream);
+
 /* Fused gather + class moments straight from the cube (the pipeline form of
  * assemble_matrix + compute_scatter): xy as for ut_gather; points outside the
  * (shard of the) cube are skipped and reported in first_bad (-1 if none). */
@@ -148,6 +155,13 @@ size_t ut_region_moments_ws(int32_t bands);
 int ut_region_moments(const ut_cube* cube, int64_t x0, int64_t y0, int64_t w,
                       int64_t h, double* moments, void* ws, size_t ws_bytes,
                       void* stream);
+/* Diagnostics for tests: the path the calling thread's last ut_region_moments
+ * took (UT_REGION_PATH_*), and the byte offset in the workspace of the int32
+ * flag the integer path raises when a sample left its fixed-point range (the
+ * fp64 path then redid the region). */
+enum { UT_REGION_PATH_DFMA = 0, UT_REGION_PATH_DMMA = 1, UT_REGION_PATH_IMMA = 2 };
+int32_t ut_region_last_path(void);
+int64_t ut_region_flag_offset(void);
 
 /* ------------------------------------------------- K3: PCA solve
  * Combines `groups` region-moment records, then std / correlation /

@@ -20,8 +20,8 @@ from .pipeline import (CvaPipeline, FolioStream, PcaPipeline, RenderResult,  # n
                        row_bounds)
 from .projection import (ALL_METHODS, METHOD_CVA, METHOD_LDA, METHOD_PCA,  # noqa: F401
                          METHOD_PCA_UNSUPERVISED, ProjectionModel, ScatterPair,
-                         compute_scatter, fit, fit_cva, fit_pca, fit_pca_unsupervised,
-                         project_stack)
+                         compute_scatter, fit, fit_cva, fit_lda, fit_pca,
+                         fit_pca_unsupervised, project_stack, standardize)
 from .quantize import code_dtype, linear_to_codes, max_code, round_half_away  # noqa: F401
 from .rendering import (PERCENTILE_CHOICES, CompositeRecipe, DeviceScorePlane,  # noqa: F401
                         RenderSpec, compose_rgb,

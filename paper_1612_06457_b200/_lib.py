@@ -21,13 +21,14 @@ if os.environ.get("UT_LIB_PATH"):  # dev: a kernel-variant build (tools/build_va
 
 UT_OK, UT_EDATA, UT_ENUMERIC, UT_ECUDA = 0, 1, 2, 3
 UT_U8, UT_U16, UT_F16, UT_F32, UT_F64 = 0, 1, 2, 3, 4
+UT_REGION_PATH_DFMA, UT_REGION_PATH_DMMA, UT_REGION_PATH_IMMA = 0, 1, 2
 INFO_OK, INFO_ASYM_A, INFO_ASYM_M, INFO_NOT_PD, INFO_NO_CONVERGE = 0, 1, 2, 3, 4
 
 # every symbol include/undertext_b200.h declares (checked by the CPU tests)
 EXPORTS = (
     "ut_version", "ut_last_error", "ut_moment_len", "ut_gather", "ut_class_moments_ws",
-    "ut_class_moments", "ut_cube_class_moments", "ut_cva_solve", "ut_gen_eig_sym", "ut_region_moments_ws",
-    "ut_region_moments", "ut_pca_solve", "ut_project_ws", "ut_project_minmax",
+    "ut_class_moments", "ut_standardize", "ut_cube_class_moments", "ut_cva_solve", "ut_gen_eig_sym", "ut_region_moments_ws",
+    "ut_region_moments", "ut_region_last_path", "ut_region_flag_offset", "ut_pca_solve", "ut_project_ws", "ut_project_minmax",
     "ut_stretch", "ut_plane_minmax_ws", "ut_plane_minmax", "ut_linear_to_codes",
     "ut_plane_select_ws", "ut_plane_select", "ut_normalize_ws", "ut_normalize_stack",
     "ut_synth_cube", "ut_class_of", "ut_encode_ws", "ut_encode_bound", "ut_encode_png",
@@ -63,11 +64,14 @@ _SIGS = {
     "ut_gather": (I32, [C.POINTER(Cube), P, I64, P, I64, P, P]),
     "ut_class_moments_ws": (SZ, [I64, I32, I32]),
     "ut_class_moments": (I32, [P, I64, P, I64, I32, I32, P, P, P, SZ, P]),
+    "ut_standardize": (I32, [P, I64, I32, I64, P, I64, P, P, P]),
     "ut_cube_class_moments": (I32, [C.POINTER(Cube), P, P, I64, I32, P, P, P, P, SZ, P]),
     "ut_cva_solve": (I32, [P, I32, I32, I32, F64, I32, C.POINTER(CvaOut), P]),
     "ut_gen_eig_sym": (I32, [P, P, I32, F64, P, P, P, P, P]),
     "ut_region_moments_ws": (SZ, [I32]),
     "ut_region_moments": (I32, [C.POINTER(Cube), I64, I64, I64, I64, P, P, SZ, P]),
+    "ut_region_last_path": (I32, []),
+    "ut_region_flag_offset": (I64, []),
     "ut_pca_solve": (I32, [P, I32, I32, C.POINTER(PcaOut), P]),
     "ut_project_ws": (SZ, []),
     "ut_project_minmax": (I32, [C.POINTER(Cube), P, I32, P, I32, P, P, I32, P, P, P, P, SZ, P]),

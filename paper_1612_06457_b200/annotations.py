@@ -106,6 +106,18 @@ class DesignMatrix:
         return {name: int(np.sum(self.labels == cid)) for cid, name in enumerate(self.class_names)}
 
 
+def point_arrays(ts) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """(xs, ys, label ids) of any training set with ``points`` of (x, y, label.id)
+    -- ours or the reference's TrainingSet (annotations.py:41-66)."""
+    if isinstance(ts, TrainingSet):
+        return ts.arrays()
+    pts = ts.points
+    n = len(pts)
+    return (np.fromiter((p.x for p in pts), dtype=np.int64, count=n),
+            np.fromiter((p.y for p in pts), dtype=np.int64, count=n),
+            np.fromiter((p.label.id for p in pts), dtype=np.int64, count=n))
+
+
 def check_points(xs, ys, width: int, row0: int, rows: int, names=None) -> None:
     """DataError for the first point outside the (shard of the) stack."""
     xs = np.asarray(xs)
@@ -137,7 +149,7 @@ def assemble_matrix(stack, ts: TrainingSet) -> DesignMatrix:
         raise DataError("assemble_matrix requires a normalized stack")
     if not ts.points:
         raise DataError("training set has no points")
-    xs, ys, ids = ts.arrays()
+    xs, ys, ids = point_arrays(ts)
     ds = on_device(stack)
     check_points(xs, ys, ds.width, ds.row0, ds.height, [p.label.name for p in ts.points])
     with torch.cuda.device(ds.planes.device):

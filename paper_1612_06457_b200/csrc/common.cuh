@@ -38,12 +38,6 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int sm_count();
 
-// 2-D tensor map over a BSQ cube slab: dim0 = pixels (contiguous), dim1 =
-// bands (stride1 bytes apart); box = box0 pixels x box1 bands, no swizzle,
-// out-of-range elements read as zero.  False (with the error set) on failure.
-bool make_tmap_2d(CUtensorMap* map, int dtype, const void* base, uint64_t dim0, uint64_t dim1,
-                  uint64_t stride1_bytes, uint32_t box0, uint32_t box1);
-
 // ---------------------------------------------------------------- samples
 template <typename T> struct Sample;
 template <> struct Sample<uint8_t>  { static constexpr int code = UT_U8;  static constexpr bool integral = true; };
@@ -189,15 +183,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // Bulk prefetch of a global range into L2 (no shared memory, no completion).
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-// One 2-D tensor-map (TMA) box copy global -> shared, completing on `bar`.
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
-                                            uint64_t* bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;

@@ -1039,7 +1039,20 @@ int launch_region(Region r, RegionWs ws, double* moments, cudaStream_t st) {
 
 using namespace ut;
 
+namespace {
+thread_local int g_region_path = -1;  // path of this thread's last ut_region_moments
+}
+
 extern "C" {
+
+int32_t ut_region_last_path(void) { return g_region_path; }
+
+int64_t ut_region_flag_offset(void) {
+  RegionWs ws;
+  char* base = reinterpret_cast<char*>(4096);
+  region_ws_layout(&ws, base);
+  return reinterpret_cast<char*>(ws.flag) - base;
+}
 
 size_t ut_region_moments_ws(int32_t bands) {
   (void)bands;
@@ -1090,6 +1103,7 @@ int ut_region_moments(const ut_cube* cube, int64_t x0, int64_t y0, int64_t w, in
   const int G_im = sm_count() < 148 ? sm_count() : 148;   // part[] holds 148 records
   const bool imma_ok = dmma_ok && region_imma_enabled(cube->bands) && cube->dtype != UT_F64 &&
                        (r.npix + kImP - 1) / kImP <= (int64_t)G_im * kImMaxWindows * kImWindowTiles;
+  g_region_path = imma_ok ? UT_REGION_PATH_IMMA : dmma_ok ? UT_REGION_PATH_DMMA : UT_REGION_PATH_DFMA;
   if (imma_ok) {
     int rc = UT_OK;
     switch (cube->dtype) {

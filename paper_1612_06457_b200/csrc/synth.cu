@@ -42,15 +42,92 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// Every floating-point step below is one IEEE-754 binary32 operation with
+// round-to-nearest (explicit __f*_rn intrinsics, so nvcc cannot contract a
+// multiply-add into an FMA), and the transcendental steps are written out as
+// fixed polynomials.  oracle/synth.py restates the generator with numpy
+// float32 arithmetic in the same order, so host and device produce the same
+// bits for every sample (tests/test_gpu_synth.py) -- the reference arm of
+// bench.py builds its sample rows on the host without this library.
+#define FADD __fadd_rn
+#define FMUL __fmul_rn
+
+// Constants are binary32 values written as hex literals (oracle/synth.py uses
+// the same bit patterns).
+// ln(u) for u in (0, 1]: u = m 2^e with m in [sqrt(1/2), sqrt(2)),
+// ln m = 2 atanh(s) = 2s + s s^2 (2/3 + s^2 (2/5 + s^2 (2/7 + s^2 2/9))),
+// s = (m - 1) / (m + 1).
+__device__ __forceinline__ float synth_log(float u) {
+  const int bits = __float_as_int(u);
+  int e = ((bits >> 23) & 0xff) - 126;
+  float m = __int_as_float((bits & 0x007fffff) | (126 << 23));  // [0.5, 1)
+  if (m < 0x1.6a09e6p-1f) {                                      // sqrt(1/2)
+    m = FMUL(m, 2.0f);
+    e -= 1;
+  }
+  const float f = FADD(m, -1.0f);
+  const float s = __fdiv_rn(f, FADD(f, 2.0f));
+  const float s2 = FMUL(s, s);
+  float p = 0x1.c71c72p-3f;                    // 2/9
+  p = FADD(0x1.24924ap-2f, FMUL(s2, p));       // 2/7
+  p = FADD(0x1.99999ap-2f, FMUL(s2, p));       // 2/5
+  p = FADD(0x1.555556p-1f, FMUL(s2, p));       // 2/3
+  const float lnm = FADD(FMUL(2.0f, s), FMUL(s, FMUL(s2, p)));
+  return FADD(FMUL((float)e, 0x1.62e43p-1f), lnm);  // e ln 2 + ln m
+}
+
+// sin and cos of x = a pi/2 for a in [0, 1): Taylor polynomials in x^2
+// (degree 13 / 14; truncation < 1e-9).
+__device__ __forceinline__ void synth_sincos_q(float a, float* s, float* c) {
+  const float x = FMUL(a, 0x1.921fb6p+0f);     // pi/2
+  const float x2 = FMUL(x, x);
+  float ps = -0x1.612462p-33f;                 // -1/13!
+  ps = FADD(0x1.ae6456p-26f, FMUL(x2, ps));    //  1/11!
+  ps = FADD(-0x1.71de3ap-19f, FMUL(x2, ps));   // -1/9!
+  ps = FADD(0x1.a01a02p-13f, FMUL(x2, ps));    //  1/7!
+  ps = FADD(-0x1.111112p-7f, FMUL(x2, ps));    // -1/5!
+  ps = FADD(0x1.555556p-3f, FMUL(x2, ps));     //  1/3!
+  *s = FADD(x, -FMUL(x, FMUL(x2, ps)));
+  float pc = -0x1.93974ap-37f;                 // -1/14!
+  pc = FADD(0x1.1eed8ep-29f, FMUL(x2, pc));    //  1/12!
+  pc = FADD(-0x1.27e4fcp-22f, FMUL(x2, pc));   // -1/10!
+  pc = FADD(0x1.a01a02p-16f, FMUL(x2, pc));    //  1/8!
+  pc = FADD(-0x1.6c16c2p-10f, FMUL(x2, pc));   // -1/6!
+  pc = FADD(0x1.555556p-5f, FMUL(x2, pc));     //  1/4!
+  pc = FADD(-0.5f, FMUL(x2, pc));              // -1/2!
+  *c = FADD(1.0f, FMUL(x2, pc));
+}
+
+// Two standard normals from one 64-bit hash (Box-Muller): u1 = (2k+1) 2^-24
+// from the top 23 bits, u2 = j 2^-24 from the low 24 bits (exact in binary32).
+__device__ __forceinline__ void synth_normal_pair(uint64_t h, float* z0, float* z1) {
+  const float u1 = FMUL((float)(uint32_t)(2u * (uint32_t)(h >> 41) + 1u), 0x1p-24f);
+  const float u2 = FMUL((float)(uint32_t)(h & 0xffffffu), 0x1p-24f);
+  const float r = __fsqrt_rn(FMUL(-2.0f, synth_log(u1)));
+  const float t = FMUL(u2, 4.0f);
+  const float q = floorf(t);
+  float s, c;
+  synth_sincos_q(FADD(t, -q), &s, &c);
+  float sn, cs;
+  switch ((int)q & 3) {
+    case 0: sn = s; cs = c; break;
+    case 1: sn = c; cs = -s; break;
+    case 2: sn = -s; cs = -c; break;
+    default: sn = -c; cs = s; break;
+  }
+  *z0 = FMUL(r, cs);
+  *z1 = FMUL(r, sn);
+}
+
 template <typename T> __device__ __forceinline__ T cast_sample(float v);
 template <> __device__ __forceinline__ float cast_sample<float>(float v) { return v; }
 template <> __device__ __forceinline__ double cast_sample<double>(float v) { return (double)v; }
 template <> __device__ __forceinline__ __half cast_sample<__half>(float v) { return __float2half_rn(v); }
 template <> __device__ __forceinline__ uint16_t cast_sample<uint16_t>(float v) {
-  return (uint16_t)floorf(4095.0f * v + 0.5f);  // round_half_away, v >= 0
+  return (uint16_t)floorf(FADD(FMUL(4095.0f, v), 0.5f));  // round_half_away, v >= 0
 }
 template <> __device__ __forceinline__ uint8_t cast_sample<uint8_t>(float v) {
-  return (uint8_t)floorf(255.0f * v + 0.5f);
+  return (uint8_t)floorf(FADD(FMUL(255.0f, v), 0.5f));
 }
 
 template <typename T>
@@ -76,27 +153,23 @@ synth_kernel(T* __restrict__ out, int64_t bs, int64_t rs, int64_t rows, int64_t 
     const uint64_t gpix = (uint64_t)gy * (uint64_t)cols + (uint64_t)x;
     float z[kMaxBands];
 #pragma unroll
-    for (int b = 0; b < kMaxBands; b += 2) {
-      const uint64_t h = splitmix64(seed ^ (gpix * 0x100000001B3ull + (uint64_t)b));
-      const float u1 = ((float)(uint32_t)(h >> 32) + 0.5f) * 2.3283064365386963e-10f;
-      const float u2 = (float)(uint32_t)h * 2.3283064365386963e-10f;
-      const float r = sqrtf(-2.0f * logf(u1));
-      float sv, cv;
-      sincospif(2.0f * u2, &sv, &cv);
-      z[b] = r * cv;
-      z[b + 1] = r * sv;
-    }
+    for (int b = 0; b < kMaxBands; b += 2)
+      synth_normal_pair(splitmix64(seed ^ (gpix * 0x100000001B3ull + (uint64_t)b)), &z[b],
+                        &z[b + 1]);
     T* dst = out + y * rs + x;
     for (int b = 0; b < bands; ++b) {
       float v = mu[c][b];
 #pragma unroll
       for (int q = 0; q < kMaxBands; ++q)
-        if (q <= b) v = fmaf(L[c][b][q], z[q], v);
+        if (q <= b) v = FADD(v, FMUL(L[c][b][q], z[q]));
       v = fminf(fmaxf(v, 0.0f), 1.0f);
       dst[b * bs] = cast_sample<T>(v);
     }
   }
 }
+
+#undef FADD
+#undef FMUL
 
 __global__ void class_of_kernel(Shapes sh, const int32_t* xy, int64_t n, int32_t* cls) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

@@ -9,10 +9,13 @@ return types and errors:
 * ``fit_pca(dm, k, prov)``         (:273-295)  -> K2 over the design matrix + K3
 * ``fit_pca_unsupervised(stack, region, k, prov)`` (:298-347) -> K2 + K3
 * ``project_stack(stack, model, components, workers)`` (:391-439) -> K4
+* ``standardize(dm)`` / ``fit_lda(dm, k, ridge, prov)`` (:152-169, :240-260) -> ``ut_standardize`` + K1 + K3
 * ``fit(method, ...)``             (:350-368)
 
 Host arrays in -> host arrays out (one H2D / D2H per call); ``DeviceStack`` /
-device ``DesignMatrix`` inputs keep everything in HBM.  ``ProjectionModel`` and
+device ``DesignMatrix`` inputs keep everything in HBM.  Inputs are duck-typed,
+so the reference's own DesignMatrix / SpectralStack / ScorePlane objects are
+accepted unchanged.  ``ProjectionModel`` and
 ``ScatterPair`` are the reference's types (JSON round trip included).
 """
 
@@ -234,8 +237,19 @@ class CvaDevice:
         return out
 
 
-def _design_on_device(dm: DesignMatrix, device):
-    if dm.on_device:
+def _on_device(dm) -> bool:
+    """Whether a design matrix's values live in HBM.  Duck-typed: the
+    reference's DesignMatrix (annotations.py:69-103, numpy values, no
+    ``on_device``) is accepted everywhere ours is."""
+    return isinstance(dm.values, torch.Tensor)
+
+
+def _design_device(dm):
+    return dm.values.device if _on_device(dm) else dev.require_cuda()
+
+
+def _design_on_device(dm, device):
+    if _on_device(dm):
         v = dm.values
         if v.dtype != torch.float64:
             v = v.double()
@@ -252,7 +266,7 @@ def _scatter_device(dm: DesignMatrix, ridge: float, want: int = 0):
         raise DataError(f"scatter needs at least 2 classes with points, got {len(ids)}")
     if dm.band_count > 32:
         raise DataError(f"the device path supports up to 32 bands, got {dm.band_count}")
-    device = dm.values.device if dm.on_device else dev.require_cuda()
+    device = _design_device(dm)
     with torch.cuda.device(device):
         values, ld = _design_on_device(dm, device)
         cls_d = dev.to_device(cls, device)
@@ -273,7 +287,7 @@ def _training_scores(dm: DesignMatrix, coeffs: np.ndarray, mean: np.ndarray):
     """coeffs^T (X - m) (projection.py:228); computed with the same numpy
     expression as ``ProjectionModel.apply`` so the two agree bit for bit
     (tests/test_projection.py:122-127) -- bookkeeping, not on the hot path."""
-    if dm.on_device:
+    if _on_device(dm):
         x = dm.values.double()
         c = torch.from_numpy(coeffs).to(x.device)
         m = torch.from_numpy(mean).to(x.device)
@@ -292,6 +306,46 @@ def fit_cva(dm: DesignMatrix, k: int | None = None, ridge: float = DEFAULT_RIDGE
     return ProjectionModel(method=METHOD_CVA, mean=mean, std=None, coefficients=coeffs,
                            eigenvalues=np.ascontiguousarray(h["evals"][:k]),
                            training_scores=np.ascontiguousarray(_training_scores(dm, coeffs, mean).T),
+                           provenance=provenance or {})
+
+
+def standardize(dm) -> tuple[DesignMatrix, np.ndarray, np.ndarray]:
+    """Recentre each band row to mean 0 and sample standard deviation 1
+    (projection.py:152-169): divisor N - 1, constant rows centred only with
+    std 1; N >= 2.  One device pass per row (``ut_standardize``); a host matrix
+    gives a host matrix, a device matrix stays in HBM."""
+    if dm.point_count < 2:
+        raise DataError("standardization needs at least 2 points")
+    device = _design_device(dm)
+    b, n = dm.band_count, dm.point_count
+    with torch.cuda.device(device):
+        values, ld = _design_on_device(dm, device)
+        out = torch.empty((b, n), dtype=torch.float64, device=device)
+        ms = torch.empty(2 * b, dtype=torch.float64, device=device)
+        _lib.check(_lib.lib().ut_standardize(values.data_ptr(), ld, b, n, out.data_ptr(), n,
+                                             ms.data_ptr(), ms[b:].data_ptr(),
+                                             dev.stream_handle()), "ut_standardize")
+        host_ms = ms.cpu().numpy()
+        labels = np.array(dm.labels)
+        names = tuple(dm.class_names)
+        if _on_device(dm):
+            return DesignMatrix(out, labels, names), host_ms[:b].copy(), host_ms[b:].copy()
+        return (DesignMatrix(out.cpu().numpy(), labels, names), host_ms[:b].copy(),
+                host_ms[b:].copy())
+
+
+def fit_lda(dm, k: int | None = None, ridge: float = DEFAULT_RIDGE,
+            provenance: dict | None = None) -> ProjectionModel:
+    """Two-class discriminant: the CVA core (K1 + K3) on the standardized
+    matrix (projection.py:240-260)."""
+    present = np.unique(np.asarray(dm.labels))
+    if len(present) != 2:
+        raise DataError(f"LDA requires exactly 2 classes, got {len(present)}")
+    sdm, mean, std = standardize(dm)
+    core = fit_cva(sdm, k=k, ridge=ridge)
+    return ProjectionModel(method=METHOD_LDA, mean=mean, std=std,
+                           coefficients=core.coefficients, eigenvalues=core.eigenvalues,
+                           training_scores=core.training_scores,
                            provenance=provenance or {})
 
 
@@ -323,6 +377,16 @@ class PcaDevice:
         _lib.check(L.ut_region_moments(C.byref(cube), x0, y0, w, h, self._local.data_ptr(),
                                        ws.data_ptr(), ws.numel(), dev.stream_handle()),
                    "ut_region_moments")
+
+    def region_path(self, device) -> tuple[int, int]:
+        """(path of this thread's last region pass -- _lib.UT_REGION_PATH_*, the
+        integer path's range flag: 1 if it handed the region to the fp64 path).
+        Synchronizes; diagnostics for tests."""
+        L = _lib.lib()
+        ws = dev.workspace("region_moments", L.ut_region_moments_ws(self.b), device)
+        off = int(L.ut_region_flag_offset())
+        flag = int(ws[off:off + 4].view(torch.int32).item())
+        return int(L.ut_region_last_path()), flag
 
     def solve(self):
         _lib.check(_lib.lib().ut_pca_solve(self.moments.data_ptr(), self.groups, self.b,
@@ -380,7 +444,7 @@ def fit_pca(dm: DesignMatrix, k: int | None = None,
     if dm.point_count < 2:
         raise DataError("standardization needs at least 2 points")
     k = _top_k(k, dm.band_count)
-    device = dm.values.device if dm.on_device else dev.require_cuda()
+    device = _design_device(dm)
     with torch.cuda.device(device):
         values, ld = _design_on_device(dm, device)
         cube = _lib.Cube(values.data_ptr(), _lib.UT_F64, dm.band_count, 1, dm.point_count, ld,
@@ -389,7 +453,7 @@ def fit_pca(dm: DesignMatrix, k: int | None = None,
         fit.moments_from(cube, 0, 0, dm.point_count, 1, device)
         fit.solve()
         hres = fit.host()
-    x = np.asarray(dm.values.cpu().numpy() if dm.on_device else dm.values, dtype=np.float64)
+    x = np.asarray(dm.values.cpu().numpy() if _on_device(dm) else dm.values, dtype=np.float64)
     coeffs = np.ascontiguousarray(hres["evecs"][:, :k])
     scores = coeffs.T @ ((x - hres["mean"][:, None]) / hres["std"][:, None])
     return _pca_model(hres, k, METHOD_PCA, provenance, training_scores=scores)
@@ -400,12 +464,12 @@ def fit(method: str, dm: DesignMatrix | None = None, stack=None, region=None, k=
     """Dispatch a fit by method tag (projection.py:350-368)."""
     if method == METHOD_CVA:
         return fit_cva(dm, k=k, ridge=ridge, provenance=provenance)
+    if method == METHOD_LDA:
+        return fit_lda(dm, k=k, ridge=ridge, provenance=provenance)
     if method == METHOD_PCA:
         return fit_pca(dm, k=k, provenance=provenance)
     if method == METHOD_PCA_UNSUPERVISED:
         return fit_pca_unsupervised(stack, region=region, k=k, provenance=provenance)
-    if method == METHOD_LDA:
-        raise DataError("LDA is outside the B200 hot path; use the reference package")
     raise DataError(f"unknown method {method!r}; expected one of {ALL_METHODS}")
 
 

@@ -124,6 +124,17 @@ class DeviceScorePlane:
         return ScorePlane(self.values.double().cpu().numpy())
 
 
+def host_plane(plane) -> ScorePlane:
+    """A host ScorePlane from ours, the reference's ScorePlane (rendering.py:39-60;
+    duck-typed on ``values``) or a bare 2-D array."""
+    if isinstance(plane, ScorePlane):
+        return plane
+    values = getattr(plane, "values", plane)
+    if isinstance(values, torch.Tensor):
+        values = values.double().cpu().numpy()
+    return ScorePlane(values)
+
+
 def _zeros_warning(reason: str) -> None:
     warnings.warn(f"{reason}; rendering all zeros", UndertextWarning, stacklevel=3)
 
@@ -153,8 +164,7 @@ def rescale_full(plane, depth: int = 8):
     if isinstance(plane, DeviceScorePlane):
         with torch.cuda.device(plane.scores.device):
             return stretch_planes(plane.scores, plane.minmax, depth, plane.index, 1)[0]
-    if not isinstance(plane, ScorePlane):
-        plane = ScorePlane(plane)
+    plane = host_plane(plane)
     max_code(depth)
     device = dev.require_cuda()
     v = plane.values
@@ -186,8 +196,7 @@ def _plane_on_device(plane):
         if not v.is_contiguous():
             v = v.contiguous()
         return v, dev.TORCH_TO_UT[v.dtype], tuple(v.shape), False
-    if not isinstance(plane, ScorePlane):
-        plane = ScorePlane(plane)
+    plane = host_plane(plane)
     device = dev.require_cuda()
     v = dev.to_device(plane.values, device)
     return v, _lib.UT_F64, plane.values.shape, True

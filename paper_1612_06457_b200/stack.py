@@ -82,6 +82,27 @@ class SpectralStack:
     def height(self) -> int:
         return int(self.planes.shape[1])
 
+    def band_by_id(self, band_id: int) -> np.ndarray:
+        """Plane for a band id; DataError for unknown ids (stack.py:84-89)."""
+        return _band_by_id(self, band_id)
+
+    def pixel_vector(self, x: int, y: int) -> np.ndarray:
+        """The B samples at (x, y) in band order, as float64 (stack.py:91-97)."""
+        _check_pixel(self, x, y)
+        return self.planes[:, y, x].astype(np.float64)
+
+
+def _band_by_id(stack, band_id: int):
+    for i, meta in enumerate(stack.bands):
+        if meta.band_id == band_id:
+            return stack.planes[i]
+    raise DataError(f"unknown band id {band_id}")
+
+
+def _check_pixel(stack, x: int, y: int) -> None:
+    if not (0 <= x < stack.width and 0 <= y < stack.height):
+        raise DataError(f"pixel ({x}, {y}) outside {stack.width}x{stack.height} stack")
+
 
 @dataclass(frozen=True)
 class DeviceStack:
@@ -130,6 +151,15 @@ class DeviceStack:
     def cube(self):
         return dev.cube_desc(self.planes, self.row0)
 
+    def band_by_id(self, band_id: int) -> torch.Tensor:
+        """The (rows, W) device plane of a band id (stack.py:84-89)."""
+        return _band_by_id(self, band_id)
+
+    def pixel_vector(self, x: int, y: int) -> np.ndarray:
+        """Host float64 samples at (x, local row y) in band order (stack.py:91-97)."""
+        _check_pixel(self, x, y)
+        return self.planes[:, y, x].double().cpu().numpy()
+
     @classmethod
     def from_host(cls, stack: SpectralStack, device=None) -> "DeviceStack":
         device = device or dev.require_cuda()
@@ -143,11 +173,19 @@ _cache_lock = threading.Lock()
 _device_copies: dict[int, tuple[weakref.ref, DeviceStack]] = {}
 
 
+def is_host_stack(stack) -> bool:
+    """A host cube in the reference's shape: ours or the reference's own
+    SpectralStack (stack.py:39-71) -- duck-typed on its fields."""
+    return isinstance(stack, SpectralStack) or (
+        isinstance(getattr(stack, "planes", None), np.ndarray) and hasattr(stack, "bands")
+        and hasattr(stack, "bit_depth") and hasattr(stack, "normalized"))
+
+
 def on_device(stack) -> DeviceStack:
     """The HBM copy of a stack (identity for a DeviceStack; cached H2D otherwise)."""
     if isinstance(stack, DeviceStack):
         return stack
-    if not isinstance(stack, SpectralStack):
+    if not is_host_stack(stack):
         raise DataError(f"expected a SpectralStack or DeviceStack, got {type(stack).__name__}")
     device = dev.require_cuda()
     key = id(stack.planes)
@@ -192,13 +230,13 @@ def normalize_stack(stack, scope: str = "per-band"):
     from . import _lib
     from .errors import UndertextWarning
 
-    if not isinstance(stack, (SpectralStack, DeviceStack)):
+    if not (isinstance(stack, DeviceStack) or is_host_stack(stack)):
         raise DataError(f"expected a SpectralStack or DeviceStack, got {type(stack).__name__}")
     if stack.normalized:
         raise DataError("stack is already normalized")
     if scope not in ("per-band", "global"):
         raise DataError(f"unknown normalization scope {scope!r}")
-    host = isinstance(stack, SpectralStack)
+    host = not isinstance(stack, DeviceStack)
     ds = DeviceStack.from_host(stack) if host else stack
     device = ds.planes.device
     b = ds.band_count
@@ -322,4 +360,4 @@ def crop(stack, x0: int, y0: int, width: int, height: int):
     planes = stack.planes[:, y0:y0 + height, x0:x0 + width]
     if isinstance(stack, DeviceStack):
         return DeviceStack(stack.bands, planes.contiguous(), stack.bit_depth, stack.normalized)
-    return SpectralStack(stack.bands, planes.copy(), stack.bit_depth, stack.normalized)
+    return SpectralStack(tuple(stack.bands), planes.copy(), stack.bit_depth, stack.normalized)

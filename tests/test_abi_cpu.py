@@ -12,7 +12,7 @@ HEADER = ROOT / "include" / "undertext_b200.h"
 
 def declared():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|int64_t|const char\*)\s+(ut_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|size_t|int64_t|const char\*)\s+(ut_\w+)\(", text, re.M)))
 
 
 def test_header_and_binding_agree():

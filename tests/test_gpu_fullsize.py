@@ -1,0 +1,188 @@
+"""Full-size parity at the configurations the bench metric is quoted on.
+
+The bench line's headline (cfg 4: CVA on the 16384 x 16384 x 32 fp32 cube,
+60,000 training pixels, k = 5) and its PCA companion (cfg4pca) are measured
+on the full cube; these tests check that same cube's device results against
+the CPU oracle (the numpy restatement of the reference, oracle/cva_pca.py):
+
+* CVA: the oracle fits the host-gathered training set (reference
+  projection.py:211-237) -- counts bit-exact; within / between scatter, class
+  means, grand mean and the top-5 eigenvalues to 1e-9; the kept vectors to
+  1e-6 after sign alignment; score planes on top / middle / bottom row bands
+  (oracle.project with the oracle's own model) to 1e-6 of the plane range;
+  uint8 codes bit-exact against the oracle's stretch of the device planes
+  (with the device's global min/max, itself checked against the planes).
+* PCA: the oracle runs the reference's two-pass chunked covariance over the
+  whole host cube (projection.py:298-347) -- mean, std, correlation,
+  eigenvalues to 1e-9, vectors to 1e-6; the int8 tensor-core path must be
+  the one that ran (not the fp64 fallback).
+* cfg 2 (PCA 2048 x 2048 x 16 fp32): every pixel of every plane and code.
+* cfg 3 (CVA 7216 x 5412 x 23 uint16): the fit against the oracle's.
+"""
+
+import gc
+
+import numpy as np
+import pytest
+
+import oracle
+from golden_util import align_signs, rel_close
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1612_06457_b200 as ut  # noqa: E402
+from paper_1612_06457_b200 import _lib, synthetic  # noqa: E402
+
+TOL = 1e-9
+VEC_TOL = 1e-6
+SCORE_TOL = 1e-6
+
+
+def eig_close(got, want, lam_max, tol=TOL):
+    got, want = np.asarray(got), np.asarray(want)
+    sig = np.abs(want) > 1e-6 * lam_max
+    ok_sig = np.all(np.abs(got[sig] - want[sig]) <= tol * np.abs(want[sig]))
+    ok_rest = np.all(np.abs(got[~sig] - want[~sig]) <= tol * lam_max)
+    return bool(ok_sig and ok_rest)
+
+
+def row_bands(height, n=64):
+    mid = height // 2 - n // 2
+    return [(0, n), (mid, mid + n), (height - n, height)]
+
+
+def check_planes(pipe, host_cube, ref_model, dev_coef, k):
+    """Planes on three row bands vs oracle.project with the oracle's model, and
+    codes vs the oracle's stretch of the device planes."""
+    ref_coef = ref_model["coefficients"]
+    signs = np.sign(np.sum(dev_coef[:, :k] * ref_coef[:, :k], axis=0))
+    mm = pipe.minmax.cpu().numpy()
+    for j in range(k):
+        plane = pipe.scores[j]
+        lo, hi = float(plane.min()), float(plane.max())
+        assert -float(mm[j]) == lo and float(mm[k + j]) == hi, j
+        assert hi > lo
+        for r0, r1 in row_bands(host_cube.shape[1]):
+            ref = oracle.project(np.ascontiguousarray(host_cube[:, r0:r1]), ref_model,
+                                 components=[j])[0]
+            got = plane[r0:r1].double().cpu().numpy()
+            err = float(np.abs(signs[j] * got - ref).max()) / (hi - lo)
+            assert err <= SCORE_TOL, (j, r0, err)
+            want_codes = oracle.linear_to_codes(got, lo, hi)
+            assert np.array_equal(pipe.codes[j, r0:r1].cpu().numpy(), want_codes), (j, r0)
+
+
+@pytest.fixture(scope="module")
+def cfg4_cube():
+    cfg = synthetic.CONFIGS["cfg4"]
+    scene = synthetic.make_scene(cfg)
+    stack = synthetic.generate(scene)
+    host = stack.planes.cpu().numpy()           # 34.4 GB host copy for the oracle
+    yield cfg, scene, stack, host
+    del stack, host
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+def test_cfg4_cva_full_size_vs_oracle(cfg4_cube):
+    cfg, scene, stack, host = cfg4_cube
+    pipe = ut.CvaPipeline(stack, scene.xs, scene.ys, scene.labels, k=cfg.k)
+    pipe.run()
+    torch.cuda.synchronize()
+    h = pipe.check()
+    values = host[:, scene.ys, scene.xs].astype(np.float64)     # host gather, point order
+    ref = oracle.fit_cva(values, scene.labels, k=cfg.k)
+    sp = ref["scatter"]
+    assert np.array_equal(h["counts"].astype(np.int64), np.asarray(sp["counts"], np.int64))
+    assert rel_close(h["within"], sp["within"], TOL)
+    assert rel_close(h["between"], sp["between"], TOL)
+    assert rel_close(h["class_means"], sp["class_means"], TOL)
+    assert rel_close(h["grand_mean"], sp["grand_mean"], TOL)
+    full = oracle.gen_eig_sym(sp["between"], sp["within"])
+    lam_max = float(np.abs(full[0]).max())
+    assert eig_close(h["evals"][:cfg.k], ref["eigenvalues"], lam_max)
+    dev_coef = align_signs(h["evecs"][:, :cfg.k], ref["coefficients"])
+    assert rel_close(dev_coef, ref["coefficients"], VEC_TOL)
+    check_planes(pipe, host, ref, h["evecs"], cfg.k)
+    del pipe
+    torch.cuda.empty_cache()
+
+
+def test_cfg4_pca_full_size_vs_oracle(cfg4_cube):
+    cfg, scene, stack, host = cfg4_cube
+    pipe = ut.PcaPipeline(stack, k=cfg.k)
+    pipe.run()
+    torch.cuda.synchronize()
+    path, flag = pipe.fit.region_path(stack.planes.device)
+    assert path == _lib.UT_REGION_PATH_IMMA and flag == 0, (path, flag)
+    h = pipe.check()
+    b = cfg.bands
+    ref = oracle.fit_pca_unsupervised(host, k=b)              # all eigenpairs
+    n = cfg.pixels
+    ref_corr = ref["gram"] / (n - 1) / np.outer(ref["std"], ref["std"])
+    assert rel_close(h["mean"], ref["mean"], TOL)
+    assert rel_close(h["std"], ref["std"], TOL)
+    assert rel_close(h["corr"], ref_corr, TOL)
+    lam_max = float(ref["eigenvalues"][0])
+    assert eig_close(h["evals"], ref["eigenvalues"], lam_max)
+    ref_k = {"mean": ref["mean"], "std": ref["std"],
+             "coefficients": ref["coefficients"][:, :cfg.k]}
+    dev_coef = align_signs(h["evecs"][:, :cfg.k], ref_k["coefficients"])
+    assert rel_close(dev_coef, ref_k["coefficients"], VEC_TOL)
+    check_planes(pipe, host, ref_k, h["evecs"], cfg.k)
+    del pipe
+    torch.cuda.empty_cache()
+
+
+def test_cfg2_pca_whole_image_vs_oracle():
+    cfg = synthetic.CONFIGS["cfg2"]
+    scene = synthetic.make_scene(cfg)
+    stack = synthetic.generate(scene)
+    host = stack.planes.cpu().numpy()
+    pipe = ut.PcaPipeline(stack, k=cfg.k)
+    codes = pipe.run().cpu().numpy()
+    path, flag = pipe.fit.region_path(stack.planes.device)
+    assert path in (_lib.UT_REGION_PATH_DMMA, _lib.UT_REGION_PATH_IMMA) and flag == 0
+    model = pipe.model()
+    ref_model, ref_scores, ref_codes = oracle.cpu_pca_pipeline(host, k=cfg.k, workers=8)
+    assert rel_close(model.mean, ref_model["mean"], TOL)
+    assert rel_close(model.std, ref_model["std"], TOL)
+    assert eig_close(model.eigenvalues, ref_model["eigenvalues"],
+                     float(ref_model["eigenvalues"][0]))
+    coef = align_signs(model.coefficients, ref_model["coefficients"])
+    assert rel_close(coef, ref_model["coefficients"], VEC_TOL)
+    scores = pipe.scores.double().cpu().numpy()
+    for j in range(cfg.k):
+        s = float(np.sign(model.coefficients[:, j] @ ref_model["coefficients"][:, j]))
+        rng = float(ref_scores[j].max() - ref_scores[j].min())
+        assert float(np.abs(s * scores[j] - ref_scores[j]).max()) / rng <= SCORE_TOL, j
+        mine = oracle.rescale_full(scores[j])
+        assert np.array_equal(codes[j], mine), j
+        want = ref_codes[j] if s > 0 else oracle.rescale_full(-ref_scores[j])
+        assert int(np.abs(codes[j].astype(int) - want.astype(int)).max()) <= 1, j
+
+
+def test_cfg3_fit_full_size_vs_oracle():
+    cfg = synthetic.CONFIGS["cfg3"]
+    scene = synthetic.make_scene(cfg)
+    stack = synthetic.generate(scene)
+    pipe = ut.CvaPipeline(stack, scene.xs, scene.ys, scene.labels, k=cfg.k)
+    pipe.run()
+    h = pipe.check()
+    xy = torch.from_numpy(np.stack([scene.xs, scene.ys], 1).astype(np.int32)).cuda()
+    gathered, bad = ut.annotations.gather(stack, xy, len(scene.xs))
+    values = gathered.cpu().numpy()
+    assert int(bad.item()) == -1
+    ref = oracle.fit_cva(values, scene.labels, k=cfg.k)
+    sp = ref["scatter"]
+    assert np.array_equal(h["counts"].astype(np.int64), np.asarray(sp["counts"], np.int64))
+    for key in ("within", "between", "class_means", "grand_mean"):
+        assert rel_close(h[key], sp[key], TOL), key
+    full = oracle.gen_eig_sym(sp["between"], sp["within"])
+    assert eig_close(h["evals"][:cfg.k], ref["eigenvalues"], float(np.abs(full[0]).max()))
+    assert rel_close(align_signs(h["evecs"][:, :cfg.k], ref["coefficients"]),
+                     ref["coefficients"], VEC_TOL)
