@@ -511,7 +511,10 @@ def run_b200(args):
     peak, peak_src = hbm_peak()
     local_px = stack.pixels
     per_px = cfg.bytes_per_pixel()
-    achieved = per_px * local_px / (k4_ms * 1e-3) / 1e9
+    # K4's own algorithmic bytes: one read of the cube (B * s per pixel); the
+    # K uint8 codes of the step's 133 B/px are written by K5, not K4
+    k4_px = cfg.bands * cfg.sample_bytes
+    achieved = k4_px * local_px / (k4_ms * 1e-3) / 1e9
     step_achieved = per_px * local_px / (ms_step * 1e-3) / 1e9
 
     traffic = None
@@ -630,10 +633,10 @@ def run_b200(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "kernel": "project_kernel (K4)",
-                         "kernel_ms": round(k4_ms, 4), "bytes_per_px": per_px,
+                         "kernel_ms": round(k4_ms, 4), "bytes_per_px": k4_px,
                          "peak_source": peak_src},
-            "roofline_step": {"achieved": round(step_achieved, 1), "frac":
-                              round(step_achieved / peak, 4),
+            "roofline_step": {"bytes_per_px": per_px, "achieved": round(step_achieved, 1),
+                              "frac": round(step_achieved / peak, 4),
                               "split_ms": {"fit": round(fit_ms, 4), "project": round(k4_ms, 4),
                                            "minmax+stretch": round(tail_ms, 4)}},
             "clocks": clocks.summary(),

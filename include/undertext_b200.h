@@ -85,6 +85,9 @@ typedef struct {
 
 /* ---------------------------------------------------------------- misc */
 int ut_version(void);
+/* SHA-256 prefix (32 hex digits) of the sources this library was built from
+ * (paper_1612_06457_b200/build.py: source_hash); the loader refuses a mismatch. */
+const char* ut_build_hash(void);
 const char* ut_last_error(void);
 /* number of doubles in one class-moment record: 1 + B + B*B */
 int64_t ut_moment_len(int32_t bands);
@@ -286,6 +289,27 @@ int ut_decode_strips(const uint8_t* src, const int64_t* in_off, const int64_t* i
                      int32_t* status, void* stream);
 int ut_unpredict(void* img, int32_t depth, int64_t rows, int64_t cols, int32_t channels,
                  int32_t predictor, int32_t swap_bytes, void* stream);
+
+/* ------------------------------------------------- collectives (row shards)
+ * SURVEY.md §8(b) ut_allreduce_f64 / §8(e): the sharded path's two exchange
+ * steps, issued as NCCL collectives on the caller's stream so a rank's step
+ * (kernels + collectives) is one capturable stream of work.  Replaces the
+ * reference's single-process numpy reductions (projection.py:186-199 -- the
+ * per-class sums -- and rendering.py:126-127 -- the global min / max), which
+ * have no multi-process form.  NCCL is loaded at run time (torch's
+ * libnccl.so.2, or UT_NCCL_LIB); ut_comm_available returns its version code
+ * or 0.  comm: the handle ut_comm_init returns (an ncclComm_t); id: 128 bytes
+ * from ut_comm_unique_id on one rank, shared by the caller (e.g. over the
+ * torch.distributed store).  op: UT_OP_SUM / UT_OP_MIN / UT_OP_MAX, in place.
+ * ut_allgather_f64: recv[r*n .. r*n+n) = rank r's send[0..n). */
+enum { UT_OP_SUM = 0, UT_OP_MIN = 1, UT_OP_MAX = 2 };
+int32_t ut_comm_available(void);
+int ut_comm_unique_id(void* id_out);
+int ut_comm_init(const void* id, int32_t nranks, int32_t rank, int32_t device, void** comm_out);
+int ut_comm_destroy(void* comm);
+int ut_allreduce_f64(void* comm, double* buf, int64_t n, int32_t op, void* stream);
+int ut_allreduce_f32(void* comm, float* buf, int64_t n, int32_t op, void* stream);
+int ut_allgather_f64(void* comm, const double* send, double* recv, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

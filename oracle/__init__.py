@@ -24,6 +24,7 @@ from .cva_pca import (  # noqa: F401
     cpu_cva_pipeline,
     cpu_pca_pipeline,
     fit_cva,
+    fit_lda,
     fit_pca_unsupervised,
     gen_eig_sym,
     linear_to_codes,
@@ -37,4 +38,5 @@ from .cva_pca import (  # noqa: F401
     round_half_away,
     scatter,
     sign_normalize,
+    standardize,
 )

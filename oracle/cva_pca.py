@@ -258,6 +258,30 @@ def fit_cva(values, labels, k=None, ridge: float = RIDGE_DEFAULT) -> dict:
     }
 
 
+def standardize(values):
+    """projection.py:152-169 -- rows to mean 0 and sample std 1 (divisor N-1);
+    constant rows are centred only, their std recorded as 1."""
+    values = np.asarray(values, dtype=np.float64)
+    if values.shape[1] < 2:
+        raise OracleError("standardization needs at least 2 points")
+    mean = values.mean(axis=1)
+    centered = values - mean[:, None]
+    var = (centered * centered).sum(axis=1) / (values.shape[1] - 1)
+    std = np.sqrt(var)
+    std[std == 0.0] = 1.0
+    return centered / std[:, None], mean, std
+
+
+def fit_lda(values, labels, k=None, ridge: float = RIDGE_DEFAULT) -> dict:
+    """projection.py:240-260 -- two-class discriminant: CVA on standardized rows."""
+    if len(np.unique(np.asarray(labels))) != 2:
+        raise OracleError("LDA requires exactly 2 classes")
+    sv, mean, std = standardize(values)
+    core = fit_cva(sv, labels, k=k, ridge=ridge)
+    core.update(method="lda", mean=mean, std=std)
+    return core
+
+
 def _pca_eig(cov, k):
     """projection.py:263-270."""
     cov = (cov + cov.T) / 2.0

@@ -26,14 +26,17 @@ INFO_OK, INFO_ASYM_A, INFO_ASYM_M, INFO_NOT_PD, INFO_NO_CONVERGE = 0, 1, 2, 3, 4
 
 # every symbol include/undertext_b200.h declares (checked by the CPU tests)
 EXPORTS = (
-    "ut_version", "ut_last_error", "ut_moment_len", "ut_gather", "ut_class_moments_ws",
+    "ut_version", "ut_build_hash", "ut_last_error", "ut_moment_len", "ut_gather", "ut_class_moments_ws",
     "ut_class_moments", "ut_standardize", "ut_cube_class_moments", "ut_cva_solve", "ut_gen_eig_sym", "ut_region_moments_ws",
     "ut_region_moments", "ut_region_last_path", "ut_region_flag_offset", "ut_pca_solve", "ut_project_ws", "ut_project_minmax",
     "ut_stretch", "ut_plane_minmax_ws", "ut_plane_minmax", "ut_linear_to_codes",
     "ut_plane_select_ws", "ut_plane_select", "ut_normalize_ws", "ut_normalize_stack",
     "ut_synth_cube", "ut_class_of", "ut_encode_ws", "ut_encode_bound", "ut_encode_png",
     "ut_encode_tiff", "ut_compose_rgb", "ut_decode_strips", "ut_unpredict",
+    "ut_comm_available", "ut_comm_unique_id", "ut_comm_init", "ut_comm_destroy",
+    "ut_allreduce_f64", "ut_allreduce_f32", "ut_allgather_f64",
 )
+UT_OP_SUM, UT_OP_MIN, UT_OP_MAX = 0, 1, 2
 
 
 class Cube(C.Structure):
@@ -59,6 +62,7 @@ I32, I64, SZ, F64 = C.c_int32, C.c_int64, C.c_size_t, C.c_double
 
 _SIGS = {
     "ut_version": (I32, []),
+    "ut_build_hash": (C.c_char_p, []),
     "ut_last_error": (C.c_char_p, []),
     "ut_moment_len": (I64, [I32]),
     "ut_gather": (I32, [C.POINTER(Cube), P, I64, P, I64, P, P]),
@@ -92,6 +96,13 @@ _SIGS = {
     "ut_encode_bound": (I64, [I64, I64, I32, I32, I32, I64]),
     "ut_encode_png": (I32, [P, I64, I64, I32, I32, P, I64, P, P, SZ, P]),
     "ut_encode_tiff": (I32, [P, I64, I64, I32, I32, I32, I64, P, I64, P, P, P, SZ, P]),
+    "ut_comm_available": (I32, []),
+    "ut_comm_unique_id": (I32, [P]),
+    "ut_comm_init": (I32, [P, I32, I32, I32, C.POINTER(P)]),
+    "ut_comm_destroy": (I32, [P]),
+    "ut_allreduce_f64": (I32, [P, P, I64, I32, P]),
+    "ut_allreduce_f32": (I32, [P, P, I64, I32, P]),
+    "ut_allgather_f64": (I32, [P, P, P, I64, P]),
 }
 
 
@@ -106,6 +117,7 @@ def lib():
                 raise RuntimeError(
                     f"B200 library not built: {LIB_PATH} is missing "
                     "(run __graft_entry__.build()); there is no CPU fallback")
+            _check_stamp()
             handle = C.CDLL(str(LIB_PATH))
             for name, (res, args) in _SIGS.items():
                 fn = getattr(handle, name)
@@ -113,6 +125,21 @@ def lib():
                 fn.argtypes = args
             _lib = handle
     return _lib
+
+
+def _check_stamp() -> None:
+    """Refuse a library not built from the sources beside it (build provenance)."""
+    if os.environ.get("UT_LIB_PATH"):
+        return  # dev variant builds carry their own flags
+    from . import build
+
+    if not (build.CSRC.is_dir() and any(build.CSRC.glob("*.cu"))):
+        return  # installed without sources: nothing to compare against
+    want, got = build.source_hash(), build.library_hash(LIB_PATH)
+    if got != want:
+        raise RuntimeError(
+            f"B200 library {LIB_PATH} was built from other sources (stamp {got}, "
+            f"sources {want}); rebuild it with __graft_entry__.build()")
 
 
 def check(rc: int, what: str) -> None:

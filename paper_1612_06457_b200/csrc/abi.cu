@@ -1,4 +1,5 @@
-// Library-wide plumbing of the C ABI: per-thread error text, version, SM count.
+// Library-wide plumbing of the C ABI: per-thread error text, version, build stamp,
+// SM count.
 #include <cstdarg>
 
 #include "common.cuh"
@@ -28,9 +29,17 @@ int sm_count() {
 
 }  // namespace ut
 
+#ifndef UT_SOURCE_HASH
+#define UT_SOURCE_HASH "unstamped"
+#endif
+// The stamp is also kept as plain bytes so the loader can read it from the file.
+extern "C" __attribute__((used)) const char ut_build_stamp[] = "UT_SOURCE_HASH=" UT_SOURCE_HASH;
+
 extern "C" {
 
 int ut_version(void) { return 1; }
+
+const char* ut_build_hash(void) { return ut_build_stamp + 15; }
 
 const char* ut_last_error(void) { return ut::g_err; }
 

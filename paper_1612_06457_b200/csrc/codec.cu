@@ -883,13 +883,8 @@ int run_deflate(const Plan& pl, const Ws& w, int format, int bpp, uint8_t* out, 
   dp.slots = w.slots;
   dp.ulen = w.ulen;
   dp.uadler = w.uadler;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(deflate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kDeflateSmem);
-    if (e != cudaSuccess) return cuda_status(e, "deflate smem attribute");
-    attr = true;
-  }
+  static SmemAttr attr;
+  if (int rc = ensure_smem(attr, deflate_kernel, kDeflateSmem, "deflate smem attribute")) return rc;
   deflate_kernel<<<(unsigned)pl.nunits, kDThreads, kDeflateSmem, st>>>(dp);
   UT_CHECK_LAUNCH("deflate_kernel");
   FrameParams fp{};

@@ -20,6 +20,24 @@ constexpr int kMaxBands = 32;
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* where);
 
+// Dynamic shared memory above 48 KB must be opted into per kernel AND per device
+// (cudaFuncSetAttribute applies to the current device only): a per-call-site
+// cache keyed by device ordinal, so a process driving several GPUs sets it on each.
+struct SmemAttr {
+  size_t bytes[64] = {};
+};
+template <typename K>
+inline int ensure_smem(SmemAttr& a, K kern, size_t bytes, const char* what) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  size_t* slot = (dev >= 0 && dev < 64) ? &a.bytes[dev] : nullptr;
+  if (slot && *slot >= bytes) return UT_OK;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return cuda_status(e, what);
+  if (slot) *slot = bytes;
+  return UT_OK;
+}
+
 #define UT_CHECK_LAUNCH(where)                                   \
   do {                                                           \
     cudaError_t _e = cudaGetLastError();                         \

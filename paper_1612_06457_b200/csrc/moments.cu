@@ -383,14 +383,9 @@ int launch_moments(const Src& src, const int32_t* cls, int64_t n, int b, int cla
                    unsigned long long* first_bad, cudaStream_t st) {
   UT_REQUIRE(ws_bytes >= ws_bytes_for(b, classes), "class moments: workspace %zu < %zu",
              ws_bytes, ws_bytes_for(b, classes));
-  static int attr = 0;
+  static SmemAttr attr;
   const int full = (int)smem_bytes(b, classes < kMaxClasses ? classes : kMaxClasses);
-  if (attr < full) {
-    cudaError_t e = cudaFuncSetAttribute(moments_kernel<Src>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, full);
-    if (e != cudaSuccess) return cuda_status(e, "moments smem attribute");
-    attr = full;
-  }
+  if (int rc = ensure_smem(attr, moments_kernel<Src>, (size_t)full, "moments smem attribute")) return rc;
   int32_t* pivots = reinterpret_cast<int32_t*>(ws);
   double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + 256 + sizeof(int32_t) * 64);
   for (int c0 = 0; c0 < classes; c0 += kMaxClasses) {

@@ -317,13 +317,10 @@ int launch_norm(const ut_cube& c, int global, uint8_t* out, double* lohi, int32_
   if constexpr (sizeof(T) <= 2 && Sample<T>::integral) {
     constexpr int lut_bytes = 1 << (8 * sizeof(T));
     if (lut_bytes > 48 * 1024) {
-      static bool attr = false;
-      if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(norm_codes_lut_kernel<T>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, lut_bytes);
-        if (e != cudaSuccess) return cuda_status(e, "norm_codes_lut smem attribute");
-        attr = true;
-      }
+      static SmemAttr attr;
+      if (int rc = ensure_smem(attr, norm_codes_lut_kernel<T>, (size_t)lut_bytes,
+                               "norm_codes_lut smem attribute"))
+        return rc;
     }
     norm_codes_lut_kernel<T><<<dim3((unsigned)gx2, c.bands), kThreads, lut_bytes, st>>>(c, lohi, out);
     UT_CHECK_LAUNCH("norm_codes_lut_kernel");

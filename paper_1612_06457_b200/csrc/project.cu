@@ -587,13 +587,8 @@ template <typename T, int KG>
 int launch_dmma(ProjParams& p, cudaStream_t st) {
   auto kern = project_dmma_kernel<T, KG>;
   const size_t smem = dmma_smem<T>(p.bands);
-  static size_t attr = 0;
-  if (attr < smem) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return cuda_status(e, "project_dmma smem attribute");
-    attr = smem;
-  }
+  static SmemAttr attr;
+  if (int rc = ensure_smem(attr, kern, smem, "project_dmma smem attribute")) return rc;
   const int64_t ntiles = (p.npix + dmma_p<T>() - 1) / dmma_p<T>();
   int64_t grid = 2 * (int64_t)sm_count();  // two CTAs (2 x 8 consumer warps) per SM
   if (grid > ntiles) grid = ntiles;
@@ -625,13 +620,8 @@ template <typename T, int VEC, int KG, bool F64, int CONS>
 int launch_tma(ProjParams& p, cudaStream_t st) {
   auto kern = project_tma_kernel<T, VEC, KG, F64, CONS>;
   const TmaShape sh = tma_shape<T, VEC, CONS>(p.bands);
-  static size_t attr = 0;
-  if (attr < sh.smem) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sh.smem);
-    if (e != cudaSuccess) return cuda_status(e, "project_tma smem attribute");
-    attr = sh.smem;
-  }
+  static SmemAttr attr;
+  if (int rc = ensure_smem(attr, kern, sh.smem, "project_tma smem attribute")) return rc;
   const int64_t ntiles = (p.npix + sh.P - 1) / sh.P;
   int64_t grid = sm_count();
   if (grid > ntiles) grid = ntiles;
@@ -973,12 +963,8 @@ template <int DEPTH>
 int launch_stretch_tma(const float* scores, const float* minmax, int k, int ld_mm, int64_t npix,
                        void* codes, cudaStream_t st) {
   auto kern = stretch_tma_kernel<DEPTH>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK5Smem);
-    if (e != cudaSuccess) return cuda_status(e, "stretch_tma smem attribute");
-    attr = true;
-  }
+  static SmemAttr attr;
+  if (int rc = ensure_smem(attr, kern, (size_t)kK5Smem, "stretch_tma smem attribute")) return rc;
   const int64_t ntiles = ((npix + kK5P - 1) / kK5P) * k;
   int64_t grid = 2 * (int64_t)sm_count();
   if (grid > ntiles) grid = ntiles;

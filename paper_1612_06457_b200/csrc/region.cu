@@ -941,12 +941,8 @@ int launch_region_imma(const Region& r, RegionWs ws, double* moments, int G, cud
   ip.part = reinterpret_cast<long long*>(ws.part);
   auto kern = region_imma_kernel<T>;
   constexpr size_t smem = im_smem<T>();
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_status(e, "region_imma smem attribute");
-    attr = true;
-  }
+  static SmemAttr attr;
+  if (int rc = ensure_smem(attr, kern, smem, "region_imma smem attribute")) return rc;
   kern<<<G, kImThreads, smem, st>>>(ip);
   UT_CHECK_LAUNCH("region_imma_kernel");
   const int total = 1 + r.bands + r.bands * r.bands;
@@ -959,13 +955,8 @@ template <typename T, int NG>
 int launch_region_dmma_ng(RdParams& rp, double* moments, cudaStream_t st) {
   auto kern = region_dmma_kernel<T, NG>;
   const size_t smem = rd_smem<T>(rp.bands);
-  static size_t attr = 0;
-  if (attr < smem) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return cuda_status(e, "region_dmma smem attribute");
-    attr = smem;
-  }
+  static SmemAttr attr;
+  if (int rc = ensure_smem(attr, kern, smem, "region_dmma smem attribute")) return rc;
   kern<<<rp.G, kRdCons + 32, smem, st>>>(rp);
   UT_CHECK_LAUNCH("region_dmma_kernel");
   const int total = 1 + rp.bands + rp.bands * rp.bands;

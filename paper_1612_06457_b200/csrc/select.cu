@@ -379,14 +379,10 @@ int launch_select(const T* v, int64_t n, long long r0, long long r1, double* out
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
   // candidate path: sample + sort (one block), one filtering pass, radix over the candidates
-  static bool attr = false;
+  static SmemAttr attr;
   const int sample_smem = kSample * (int)sizeof(unsigned long long);
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(cand_sample_kernel<T>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sample_smem);
-    if (e != cudaSuccess) return cuda_status(e, "cand_sample smem attribute");
-    attr = true;
-  }
+  if (int rc = ensure_smem(attr, cand_sample_kernel<T>, (size_t)sample_smem, "cand_sample smem attribute"))
+    return rc;
   cand_sample_kernel<T><<<1, 1024, sample_smem, st>>>(v, n, r0, r1, ws);
   UT_CHECK_LAUNCH("cand_sample_kernel");
   cand_filter_kernel<T><<<(int)grid, kThreads, 0, st>>>(v, n, ws);

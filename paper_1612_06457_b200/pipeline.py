@@ -29,7 +29,7 @@ from . import _lib
 from . import device as dev
 from .annotations import check_points
 from .eigen import DEFAULT_RIDGE, raise_for_info
-from .errors import DataError
+from .errors import DataError, NumericError
 from .projection import (CvaDevice, PcaDevice, ProjectionModel, METHOD_CVA,
                          METHOD_PCA_UNSUPERVISED, class_index, project_device, _top_k)
 from .rendering import (CompositeRecipe, RenderSpec, _zeros_warning, compose_rgb, rescale,
@@ -49,17 +49,26 @@ def route_points(ys, row0: int, rows: int) -> np.ndarray:
 
 
 class _Sharded:
-    def __init__(self, group):
-        self.group = group
-        self.world = dist.get_world_size(group) if group is not None else 1
+    """Exchange steps of a row-sharded pipeline: through ``comm`` (the library's
+    NCCL collectives, comm.py) when given, else torch.distributed on ``group``."""
+
+    def __init__(self, group, comm=None):
+        self.group, self.comm = group, comm
+        if comm is not None:
+            self.world = comm.world
+        else:
+            self.world = dist.get_world_size(group) if group is not None else 1
         self.graph = None
 
     def capture(self):
-        """Record run() as a CUDA graph (single-GPU pipelines): the path is a
-        handful of short kernels at small sizes, so launch overhead matters.
-        Call after one eager run (it sets up workspaces and kernel attributes)."""
-        if self.world > 1:
-            raise RuntimeError("graph capture is for unsharded pipelines")
+        """Record run() as a CUDA graph: the path is a handful of short kernels at
+        small sizes, so launch overhead matters.  Sharded pipelines capture too when
+        their exchanges go through a ``Comm`` (NCCL collectives on the same stream);
+        torch.distributed collectives (gloo) cannot be captured.  Call after one
+        eager run (it sets up workspaces and kernel attributes)."""
+        if self.world > 1 and self.comm is None:
+            raise RuntimeError("graph capture of a sharded pipeline needs a Comm "
+                               "(NCCL collectives through the library)")
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
@@ -79,11 +88,15 @@ class _Sharded:
         return self.codes
 
     def gather_moments(self, fit):
-        if self.world > 1:
+        if self.comm is not None:
+            self.comm.allgather_f64(fit.local_moments(), fit.moments)
+        elif self.world > 1:
             dist.all_gather_into_tensor(fit.moments, fit.local_moments(), group=self.group)
 
     def reduce_minmax(self, minmax):
-        if self.world > 1:
+        if self.comm is not None:
+            self.comm.allreduce(minmax, "max")
+        elif self.world > 1:
             dist.all_reduce(minmax, op=dist.ReduceOp.MAX, group=self.group)
 
 
@@ -92,8 +105,8 @@ class CvaPipeline(_Sharded):
 
     def __init__(self, stack: DeviceStack, xs, ys, labels, k: int | None = None,
                  ridge: float = DEFAULT_RIDGE, precision: str | None = None, depth: int = 8,
-                 group=None):
-        super().__init__(group)
+                 group=None, comm=None):
+        super().__init__(group, comm)
         if not stack.normalized:
             raise DataError("assemble_matrix requires a normalized stack")
         self.ds = stack
@@ -113,6 +126,7 @@ class CvaPipeline(_Sharded):
         # the random gather TLB-/sector-friendly (the sums' order is fixed by
         # this permutation, so results stay deterministic)
         own = own[np.lexsort((xs[own], ys[own], cls[own]))]
+        self.own = own            # K1 order -> caller's point index (error reports)
         self.n = len(own)
         b = stack.band_count
         with torch.cuda.device(self.device):
@@ -169,6 +183,7 @@ class CvaPipeline(_Sharded):
         self.xy.copy_(xy, non_blocking=True)
         self.cls.copy_(cls, non_blocking=True)
         self.pivots.copy_(pivots, non_blocking=True)
+        self.own = None           # the swapped-in set is already in K1 order
 
     # -- the hot path -------------------------------------------------------
     def fit_only(self):
@@ -196,10 +211,18 @@ class CvaPipeline(_Sharded):
         return self.codes
 
     # -- results ------------------------------------------------------------
+    def bad_point_message(self, k1_index: int) -> str:
+        """A K1-order point index (first_bad) in the caller's terms."""
+        x, y = (int(v) for v in self.xy[k1_index].cpu())
+        if self.own is not None and k1_index < len(self.own):
+            return f"training point {int(self.own[k1_index])} at ({x}, {y}) outside the stack"
+        return f"training point at ({x}, {y}) outside the stack"
+
     def check(self):
         """Synchronize and raise the reference's errors for device-side failures."""
-        if int(self.first_bad.item()) >= 0:
-            raise DataError(f"training point {int(self.first_bad.item())} outside the stack")
+        bad = int(self.first_bad.item())
+        if bad >= 0:
+            raise DataError(self.bad_point_message(bad))
         h = self.fit.host()
         raise_for_info(h["info"], h["aux"])
         if int(self.nonfinite.item()):
@@ -221,8 +244,8 @@ class PcaPipeline(_Sharded):
     """Unsupervised PCA fit + projection + stretch of one (shard of a) device cube."""
 
     def __init__(self, stack: DeviceStack, k: int | None = None, precision: str | None = None,
-                 depth: int = 8, group=None):
-        super().__init__(group)
+                 depth: int = 8, group=None, comm=None):
+        super().__init__(group, comm)
         self.ds = stack
         self.device = stack.planes.device
         self.k = _top_k(k, stack.band_count)
@@ -308,6 +331,16 @@ class FolioStream:
         shape = tuple(cubes[0].shape)
         if any(tuple(c.shape) != shape or c.dtype != cubes[0].dtype for c in cubes):
             raise DataError("all folios of a stream must share shape and sample type")
+        # every folio's points are validated here, on the host: K1 drops an
+        # out-of-range point (flagging it), and a later folio would overwrite the flag
+        for i, tr in enumerate(training):
+            xy = np.asarray(tr[0].cpu() if torch.is_tensor(tr[0]) else tr[0])
+            if xy.ndim != 2 or xy.shape[1] != 2:
+                raise DataError(f"folio {i}: training xy must be (n, 2), got {xy.shape}")
+            try:
+                check_points(xy[:, 0], xy[:, 1], shape[2], 0, shape[1])
+            except DataError as exc:
+                raise DataError(f"folio {i}: {exc}") from None
         self.bufs, self.pipes = [], []
         xy0, cls0, _ = (t.numpy() for t in training[0])
         for _ in range(2):
@@ -318,6 +351,11 @@ class FolioStream:
             self.pipes.append(CvaPipeline(ds, xy0[:, 0], xy0[:, 1], cls0, k=k,
                                           precision=precision, depth=depth))
         self.copy_stream = torch.cuda.Stream(self.device)
+        # per-folio device status, copied out of the pipeline after each folio
+        # (each run resets first_bad / info / nonfinite): [first_bad, info, nonfinite]
+        b = shape[0]
+        self.status = torch.zeros((len(cubes), 3), dtype=torch.int64, device=self.device)
+        self.aux = torch.zeros((len(cubes), b), dtype=torch.float64, device=self.device)
 
     def launches(self) -> int:
         return self.pipes[0].launches() * len(self.cubes)
@@ -336,23 +374,46 @@ class FolioStream:
                 self.pipes[j].load_training(*self.training[i])
                 ready.record(self.copy_stream)
             comp.wait_event(ready)
-            self.pipes[j].run()
-            self.outs[i].copy_(self.pipes[j].codes, non_blocking=True)
+            p = self.pipes[j]
+            p.run()
+            self.outs[i].copy_(p.codes, non_blocking=True)
+            self.status[i, 0:1].copy_(p.first_bad)
+            self.status[i, 1:2].copy_(p.fit.info)
+            self.status[i, 2:3].copy_(p.nonfinite)
+            self.aux[i].copy_(p.fit.views["aux"])
             done[j] = torch.cuda.Event()
             done[j].record(comp)
         # the copy stream must not run ahead into buffers the caller reuses
         self.copy_stream.wait_stream(comp)
 
     def check(self):
-        for p in self.pipes:
-            p.check()
+        """Raise the first failing folio's error (with its index)."""
+        status = self.status.cpu().numpy()
+        for i, (bad, info, nonfinite) in enumerate(status):
+            try:
+                if bad >= 0 and self.training[i][0].shape[0] > int(bad):
+                    x, y = (int(v) for v in self.training[i][0][int(bad)])
+                    raise DataError(f"training point at ({x}, {y}) outside the stack")
+                raise_for_info(int(info), self.aux[i].cpu().numpy())
+                if nonfinite:
+                    raise DataError("score plane contains NaN or Inf")
+            except (DataError, NumericError) as exc:
+                raise type(exc)(f"folio {i}: {exc}") from None
 
 
 # ------------------------------------------------------------ render_planes
-# Components projected per K4 pass (the kernel's limit); the reference batches
-# 8 planes at a time to bound host memory (pipeline.py:44), re-reading the
-# cube once per batch.
+# Components projected per K4 pass: up to 32 (the kernel's limit, one cube read
+# for all of them) when their fp32 score planes and codes fit in half the free
+# HBM; fewer otherwise.  The reference batches 8 planes at a time to bound host
+# memory (pipeline.py:44), re-reading the cube once per batch.
 _RENDER_BATCH = 32
+
+
+def _render_batch(ds, n_specs: int, depth_bytes: int = 2) -> int:
+    npix = ds.height * ds.width
+    per_component = npix * (4 + n_specs * depth_bytes)
+    free, _ = torch.cuda.mem_get_info(ds.planes.device)
+    return int(max(1, min(_RENDER_BATCH, (free // 2) // max(per_component, 1))))
 
 
 @dataclass
@@ -399,8 +460,9 @@ def render_planes(stack, model: ProjectionModel, specs: list[RenderSpec], out_di
     result = RenderResult()
     needed = set() if recipe is None else {recipe.red, recipe.green, recipe.blue}
     recipe_planes: dict = {}
-    for i in range(0, len(components), _RENDER_BATCH):
-        batch = components[i:i + _RENDER_BATCH]
+    step = _render_batch(ds, len(specs))
+    for i in range(0, len(components), step):
+        batch = components[i:i + step]
         planes = project_stack(ds, model, components=batch, workers=workers)
         ranges = planes[0].minmax.cpu().numpy()   # [-min_0.., max_0..] of the batch
         nb = len(batch)

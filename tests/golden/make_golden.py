@@ -32,7 +32,7 @@ from undertext.annotations import (  # noqa: E402
 )
 from undertext.eigen import solve_gen_eig_sym  # noqa: E402
 from undertext.projection import (  # noqa: E402
-    compute_scatter, fit_cva, fit_pca_unsupervised, project_stack,
+    compute_scatter, fit_cva, fit_lda, fit_pca_unsupervised, project_stack, standardize,
 )
 from undertext.projection import ProjectionModel  # noqa: E402
 from undertext.rendering import (ScorePlane, rescale_full, rescale_percentile,  # noqa: E402
@@ -213,7 +213,32 @@ def rescale_mode_cases():
     np.savez_compressed(HERE / "rescale_modes.npz", **out)
 
 
+def lda_cases():
+    """fit_lda / standardize (projection.py:152-169, :240-260) on two-class sets,
+    incl. a constant band (std recorded as 1)."""
+    out = {}
+    rng = np.random.default_rng(4242)
+    cases = []
+    for b, n in [(6, 30), (16, 50), (32, 80)]:
+        v, l = random_labeled(rng, b, 2, n)
+        cases.append((np.asarray(v, dtype=np.float64), np.asarray(l)))
+    v, l = random_labeled(rng, 5, 2, 12)
+    v = np.asarray(v, dtype=np.float64).copy()
+    v[2] = 0.375
+    cases.append((v, np.array([3, 8])[np.asarray(l)]))
+    for i, (v, l) in enumerate(cases):
+        dm = DesignMatrix(v, np.asarray(l, dtype=np.intp), tuple())
+        sdm, mean, std = standardize(dm)
+        m = fit_lda(dm, k=1)
+        out.update({f"{i}_values": v, f"{i}_labels": l, f"{i}_std_values": sdm.values,
+                    f"{i}_mean": mean, f"{i}_std": std, f"{i}_coef": m.coefficients,
+                    f"{i}_evals": m.eigenvalues, f"{i}_scores": m.training_scores})
+    out["n"] = np.array(len(cases))
+    np.savez_compressed(HERE / "lda.npz", **out)
+
+
 if __name__ == "__main__":
+    lda_cases()
     scatter_cases()
     eigen_cases()
     cube_case("cva_f64", 48, 64, 16, 3, np.float64, 11, 60, 2, 8)

@@ -219,3 +219,63 @@ def test_folio_stream_matches_independent_pipelines():
             assert np.array_equal(o.numpy(), w)
     with pytest.raises(ut.DataError):
         fs.pipes[0].load_training(train[0][0][:5], train[0][1][:5], train[0][2])
+
+
+def _folios(n, nan_folio=None):
+    from dataclasses import replace
+
+    from paper_1612_06457_b200 import synthetic
+
+    base = synthetic.scaled(synthetic.CONFIGS["cfg5"], 120, 96, 40)
+    cubes, train, outs = [], [], []
+    for f in range(n):
+        sc = synthetic.make_scene(replace(base, seed=91 + f))
+        planes = synthetic.generate(sc).planes.cpu()
+        if f == nan_folio:
+            planes[0, 7, 9] = float("nan")
+        cubes.append(planes.pin_memory())
+        arrs = ut.CvaPipeline.training_arrays(sc.xs, sc.ys, sc.labels)
+        train.append(tuple(torch.from_numpy(a).pin_memory() for a in arrs))
+        outs.append(torch.empty((base.k, base.height, base.width), dtype=torch.uint8,
+                                pin_memory=True))
+    return base, cubes, train, outs
+
+
+def test_folio_stream_reports_the_failing_folio():
+    """an earlier folio's device error must survive later folios that
+    reuse its buffer -- per-folio status slots, reported with the folio index."""
+    _, cubes, train, outs = _folios(4, nan_folio=0)
+    fs = ut.FolioStream(cubes, train, outs, k=3)
+    fs.run()
+    torch.cuda.synchronize()
+    with pytest.raises(ut.DataError, match=r"folio 0: score plane contains NaN"):
+        fs.check()
+
+
+def test_folio_stream_validates_every_training_set():
+    _, cubes, train, outs = _folios(3)
+    xy, cls, piv = train[2]
+    bad = xy.clone()
+    bad[5, 1] = 10_000
+    train[2] = (bad, cls, piv)
+    with pytest.raises(ut.DataError, match=r"folio 2: .*outside"):
+        ut.FolioStream(cubes, train, outs, k=3)
+
+
+def test_bad_point_reported_in_caller_order():
+    """A point swapped in past the stack: K1 flags it; check() names it by its
+    coordinates (K1's class-sorted index is not the caller's)."""
+    rng = np.random.default_rng(12)
+    cube, _ = cube_of(rng, 6, 40, 50, np.float32)
+    xs = rng.integers(0, 50, 30)
+    ys = rng.integers(0, 40, 30)
+    labels = np.arange(30) % 3
+    st = ut.DeviceStack(ut.stack.default_bands(6), torch.from_numpy(cube).cuda(), 8, True)
+    pipe = ut.CvaPipeline(st, xs, ys, labels, k=2)
+    xy, cls, piv = ut.CvaPipeline.training_arrays(xs, ys, labels)
+    xy[4] = (51, 3)
+    pipe.load_training(torch.from_numpy(xy).cuda(), torch.from_numpy(cls).cuda(),
+                       torch.from_numpy(piv).cuda())
+    pipe.run()
+    with pytest.raises(ut.DataError, match=r"\(51, 3\) outside"):
+        pipe.check()

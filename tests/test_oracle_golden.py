@@ -173,3 +173,18 @@ def test_rescale_modes_golden():
     assert np.array_equal(oracle.rescale_percentile(g["lin"], 5.0), g["lin_p5"])
     flat = np.sort(np.random.default_rng(1).normal(size=1000))
     assert oracle.nearest_rank(flat, 1.0) == flat[9] and oracle.nearest_rank(flat, 99.0) == flat[989]
+
+
+def test_lda_golden():
+    """standardize + fit_lda (projection.py:152-169, :240-260) vs the reference,
+    incl. a constant band (std 1) and non-contiguous label ids."""
+    g = load("lda")
+    for i in range(int(g["n"])):
+        sv, mean, std = oracle.standardize(g[f"{i}_values"])
+        assert rel_close(sv, g[f"{i}_std_values"], 1e-12), i
+        assert rel_close(mean, g[f"{i}_mean"], 1e-12), i
+        assert rel_close(std, g[f"{i}_std"], 1e-12), i
+        m = oracle.fit_lda(g[f"{i}_values"], g[f"{i}_labels"], k=1)
+        assert rel_close(m["eigenvalues"], g[f"{i}_evals"], 1e-10), i
+        assert rel_close(m["coefficients"], g[f"{i}_coef"], 1e-8), i
+        assert rel_close(m["training_scores"], g[f"{i}_scores"], 1e-8), i
