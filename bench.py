@@ -385,10 +385,10 @@ def run_folios(args):
     return 0
 
 
-def pca_companion(ut, stack, cfg, args, group, world, stream):
+def pca_companion(ut, stack, cfg, args, group, world, stream, comm=None):
     import torch
 
-    pipe = ut.PcaPipeline(stack, k=cfg.k, precision=args.precision, group=group)
+    pipe = ut.PcaPipeline(stack, k=cfg.k, precision=args.precision, group=group, comm=comm)
     for _ in range(3):
         pipe.run()
     torch.cuda.synchronize()
@@ -429,6 +429,65 @@ def pca_companion(ut, stack, cfg, args, group, world, stream):
     return out
 
 
+def sharded_self_check(ut, synthetic, base, group, comm, world, rank):
+    """N > 1, before timing: this run's sharded pipelines and collectives on a
+    small cube of the workload's generator vs an unsharded fit of the same cube
+    on rank 0.  Models to SURVEY Appendix A (eigenvalues 1e-9 relative, kept
+    vectors 1e-6 after sign alignment), uint8 codes of rank 0's rows within 1
+    (global min/max through the MAX exchange).  Every rank exits if it fails:
+    no number is printed for a wrong multi-GPU result."""
+    import torch
+    import torch.distributed as dist
+
+    cfg = synthetic.scaled(base, 64 * world, 384, per_class=400)
+    scene = synthetic.make_scene(cfg)
+    r0, r1 = ut.row_bounds(cfg.height, world, rank)
+    shard = synthetic.generate(scene, row0=r0, rows=r1 - r0)
+    full = synthetic.generate(scene) if rank == 0 else None
+    report, ok_all = {}, True
+    for method in ("cva", "pca"):
+        def make(st, sharded):
+            kw = dict(group=group, comm=comm) if sharded else {}
+            if method == "cva":
+                return ut.CvaPipeline(st, scene.xs, scene.ys, scene.labels, k=cfg.k, **kw)
+            return ut.PcaPipeline(st, k=cfg.k, **kw)
+
+        sp = make(shard, True)
+        codes = sp.run()
+        torch.cuda.synchronize()
+        m = sp.model()
+        ok, detail = True, {}
+        if rank == 0:
+            up = make(full, False)
+            want = up.run()
+            um = up.model()
+            lam = float(np.abs(m.eigenvalues - um.eigenvalues).max() /
+                        max(np.abs(um.eigenvalues).max(), 1e-300))
+            sign = np.sign(np.sum(m.coefficients * um.coefficients, axis=0))
+            vec = float(np.abs(m.coefficients * sign - um.coefficients).max() /
+                        max(np.abs(um.coefficients).max(), 1e-300))
+            diff = int((codes.int() - want[:, r0:r1].int()).abs().max().item())
+            ok = lam <= 1e-9 and vec <= 1e-6 and diff <= 1
+            detail = {"eigenvalue_rel": lam, "vector_rel": vec, "codes_max_diff": diff,
+                      "ok": bool(ok)}
+            del up, want
+        flag = torch.tensor([0 if ok else 1], dtype=torch.int32, device="cuda")
+        dist.broadcast(flag, src=0, group=group)
+        ok_all = ok_all and int(flag.item()) == 0
+        report[method] = detail
+        del sp, codes
+    del shard, full
+    torch.cuda.empty_cache()
+    report["collectives"] = "ut_comm (NCCL via the C ABI)" if comm is not None else \
+        f"torch.distributed ({dist.get_backend(group)})"
+    report["cube"] = f"{cfg.height}x{cfg.width}x{cfg.bands}, {world} row shards"
+    if not ok_all:
+        if rank == 0:
+            sys.stderr.write(f"sharded self-check FAILED: {json.dumps(report)}\n")
+        raise SystemExit(3)
+    return report
+
+
 def run_b200(args):
     import torch
 
@@ -436,20 +495,30 @@ def run_b200(args):
     from paper_1612_06457_b200 import synthetic
 
     world, rank, local = dist_setup(args.gpus)
-    group = None
+    group = comm = None
+    self_check = None
     if world > 1:
         import torch.distributed as dist
 
         group = dist.group.WORLD
+        # the exchange steps go through the library's NCCL collectives (C ABI)
+        # unless UT_BENCH_COMM=torch; gloo runs (one-GPU functional checks) use
+        # torch.distributed
+        if dist.get_backend(group) == "nccl" and os.environ.get("UT_BENCH_COMM", "ut") != "torch":
+            from paper_1612_06457_b200.comm import Comm
+
+            comm = Comm.from_group(group)
+        self_check = sharded_self_check(ut, synthetic, cfg_of(args), group, comm, world, rank)
     cfg = cfg_of(args)
     scene = synthetic.make_scene(cfg)
     r0, r1 = ut.row_bounds(cfg.height, world, rank)
     stack = synthetic.generate(scene, row0=r0, rows=r1 - r0)
     if cfg.method == "cva":
         pipe = ut.CvaPipeline(stack, scene.xs, scene.ys, scene.labels, k=cfg.k,
-                              precision=args.precision, group=group)
+                              precision=args.precision, group=group, comm=comm)
     else:
-        pipe = ut.PcaPipeline(stack, k=cfg.k, precision=args.precision, group=group)
+        pipe = ut.PcaPipeline(stack, k=cfg.k, precision=args.precision, group=group,
+                              comm=comm)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         pipe.run()
@@ -533,7 +602,7 @@ def run_b200(args):
     # workload): covariance (K2) + eigen + projection (K4) + stretch (K5)
     pca = None
     if cfg.method == "cva" and not args.no_pca:
-        pca = pca_companion(ut, stack, cfg, args, group, world, stream)
+        pca = pca_companion(ut, stack, cfg, args, group, world, stream, comm)
 
     # ---- e2e: host (pinned) cube in, uint8 planes out, through the same API
     e2e = None
@@ -645,7 +714,12 @@ def run_b200(args):
             "gpu_launches": launches,
             "cpu_baseline": cpu,
         }
+        if self_check is not None:
+            line["self_check"] = self_check
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        torch.cuda.synchronize()
+        comm.close()
     if world > 1:
         import torch.distributed as dist
 

@@ -168,3 +168,40 @@ class TestLoadStack:
         cv2.imwrite(str(tmp_path / "rgb.png"), np.zeros((4, 4, 3), dtype=np.uint8))
         with pytest.raises(ut.DataError, match="channel"):
             ut.load_stack(_manifest(tmp_path, ["rgb.png,365,uv"]))
+
+
+def test_measured_path_never_uses_host_codecs(monkeypatch):
+    """PNG, LZW and tiled TIFFs are decoded by cv2 exactly as the reference
+    reads them (outside the measured path).  The measured path
+    -- the cube resident in HBM, fit, projection, stretch, as bench.py times it
+    (CVA, the PCA companion and the streamed folio batch) -- must never reach a
+    host codec: every cv2 entry point is made to fail here."""
+    from dataclasses import replace
+
+    import cv2
+
+    from paper_1612_06457_b200 import synthetic
+
+    def boom(*args, **kwargs):
+        raise AssertionError("host codec called on the measured path")
+
+    for name in ("imread", "imdecode", "imwrite", "imencode", "imreadmulti"):
+        monkeypatch.setattr(cv2, name, boom)
+    cfg = synthetic.scaled(synthetic.CONFIGS["cfg4"], 128, 96, per_class=40)
+    scene = synthetic.make_scene(cfg)
+    stack = synthetic.generate(scene)
+    ut.CvaPipeline(stack, scene.xs, scene.ys, scene.labels, k=cfg.k).run()
+    ut.PcaPipeline(stack, k=cfg.k).run()
+    base = synthetic.scaled(synthetic.CONFIGS["cfg5"], 64, 48, 20)
+    cubes, train, outs = [], [], []
+    for f in range(2):
+        sc = synthetic.make_scene(replace(base, seed=5 + f))
+        cubes.append(synthetic.generate(sc).planes.cpu().pin_memory())
+        arrs = ut.CvaPipeline.training_arrays(sc.xs, sc.ys, sc.labels)
+        train.append(tuple(torch.from_numpy(a).pin_memory() for a in arrs))
+        outs.append(torch.empty((base.k, base.height, base.width), dtype=torch.uint8,
+                                pin_memory=True))
+    fs = ut.FolioStream(cubes, train, outs, k=base.k)
+    fs.run()
+    torch.cuda.synchronize()
+    fs.check()

@@ -225,8 +225,11 @@ def test_pipeline_fit_model_and_render_planes_end_to_end(tmp_path):
     dm = host_design(stack, training)
     r = oracle.fit_cva(dm.values, dm.labels, k=2)
     assert rel_close(model.eigenvalues, r["eigenvalues"], 1e-9)
-    res = bp.render_planes(stack, model, [b.RenderSpec()], tmp_path, run_name="page")
-    assert [p.name for p in res.plane_paths] == ["page_plane00.png", "page_plane01.png"]
+    spec = b.RenderSpec()
+    res = bp.render_planes(stack, model, [spec], tmp_path, run_name="page")
+    assert [p.name for p in res.plane_paths] == [bp.plane_filename("page", k, spec, "png")
+                                                 for k in range(2)]
+    assert res.plane_paths[0].name == "page_plane00_full.png"   # pipeline.py:120-125 names
     planes = b.project_stack(stack, model)
     for p, plane in zip(res.plane_paths, planes):
         img = cv2.imread(str(p), cv2.IMREAD_UNCHANGED)
