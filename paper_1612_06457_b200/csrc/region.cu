@@ -794,9 +794,16 @@ region_imma_kernel(ImParams r) {
           constexpr int V = 16 / sizeof(T);
           T x[16];
 #pragma unroll
-          for (int q = 0; q < 16 / V; ++q)
+          for (int q = 0; q < 16 / V; ++q) {
+#if defined(UT_IM_PROBE) && (UT_IM_PROBE & 1)   // dev probe: no shared-memory reads of the input
+            uint4 fake;
+            fake.x = fake.y = fake.z = fake.w = 0x3f000000u + (uint32_t)(i & 255) * 8u + (uint32_t)q;
+            *reinterpret_cast<uint4*>(x + q * V) = fake;
+#else
             *reinterpret_cast<uint4*>(x + q * V) =
                 *reinterpret_cast<const uint4*>(stage + (size_t)b * PS + 16 * cw + q * V);
+#endif
+          }
           uint32_t wd[16];
           if (valid >= 16) {  // the common case: no masks
 #pragma unroll
@@ -823,8 +830,12 @@ region_imma_kernel(ImParams r) {
           transpose4(wd[4], wd[5], wd[6], wd[7], o1);
           transpose4(wd[8], wd[9], wd[10], wd[11], o2);
           transpose4(wd[12], wd[13], wd[14], wd[15], o3);
+#if defined(UT_IM_PROBE) && (UT_IM_PROBE & 2)   // dev probe: no operand stores
+          if ((o0[0] ^ o1[1] ^ o2[2] ^ o3[3]) == 0x12345678u) dst[0] = make_uint4(o0[1], o1[2], o2[3], o3[0]);
+#else
 #pragma unroll
           for (int d = 0; d < 4; ++d) dst[32 * d] = make_uint4(o0[d], o1[d], o2[d], o3[d]);
+#endif
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
