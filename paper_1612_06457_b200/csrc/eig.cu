@@ -70,6 +70,8 @@ struct Smem {
   int flag;
   int order[N];
   int code[N];
+  double qd[N], qe[N], qc[N], qs[N];  // tridiagonal QL: diagonal, off-diagonal, rotations
+  double hu[N];                        // Householder vector
 };
 
 template <int NT> __device__ __forceinline__ void team_sync() {
@@ -276,6 +278,197 @@ __device__ int jacobi_team(Smem& s, double* a, double* v, int n) {
   return UT_INFO_NO_CONVERGE;
 }
 
+// Symmetric eigensolver for n <= 32 run by warp 0 (lane = row): Householder
+// reduction to tridiagonal form with the transformations accumulated in v
+// (Golub & Van Loan, Alg. 8.3.1), then the implicit QL iteration with
+// Wilkinson-type shifts on the tridiagonal matrix (the classic tql2 scheme),
+// its Givens rotations applied to the rows of v.  Same contract as
+// jacobi_team: on return the eigenvalues are on the diagonal of a (off-
+// diagonals zeroed) and the eigenvectors are the columns of v.  The scalar
+// QL recurrence runs on lane 0; each QL step's rotation sequence is then
+// applied by all lanes to their row of v.  O(n^3) work in ~n^2 warp steps,
+// instead of ~9 sweeps x 31 rounds x 2 block barriers of the parallel Jacobi
+// at n = 32.  Returns 0, or UT_INFO_NO_CONVERGE (the caller falls back).
+__device__ int ql_warp(Smem& s, double* a, double* v, int n) {
+  const int lane = threadIdx.x & 31;
+  for (int c = 0; c < n; ++c)
+    if (lane < n) v[lane * LD + c] = (lane == c) ? 1.0 : 0.0;
+  __syncwarp();
+  // ---- Householder: zero column k below the subdiagonal, k = 0 .. n-3
+  for (int k = 0; k + 2 < n; ++k) {
+    const double x = (lane > k && lane < n) ? a[lane * LD + k] : 0.0;
+    double ss = x * x;
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const double x1 = __shfl_sync(0xffffffffu, x, k + 1);
+    const double alpha = sqrt(ss);
+    const double beta = x1 > 0.0 ? -alpha : alpha;
+    const double h = ss - beta * x1;  // |u|^2 / 2, u = x - beta e_{k+1}
+    if (!(h > 0.0)) continue;         // column already reduced (or all zero)
+    const double u = (lane == k + 1) ? x1 - beta : x;
+    if (lane < N) s.hu[lane] = u;
+    __syncwarp();
+    // p = A u / h on the trailing block (rows, columns k+1..n-1)
+    double pr = 0.0;
+    if (lane > k && lane < n)
+      for (int c = k + 1; c < n; ++c) pr += a[lane * LD + c] * s.hu[c];
+    pr /= h;
+    double up = (lane > k && lane < n) ? u * pr : 0.0;
+    for (int o = 16; o > 0; o >>= 1) up += __shfl_xor_sync(0xffffffffu, up, o);
+    const double q = pr - (up / (2.0 * h)) * u;  // q = p - K u, K = u^T p / (2h)
+    __syncwarp();
+    if (lane < N) s.qs[lane] = q;
+    __syncwarp();
+    if (lane > k && lane < n)
+      for (int c = k + 1; c < n; ++c) a[lane * LD + c] -= u * s.qs[c] + q * s.hu[c];
+    // column / row k: (beta, 0, ..., 0)
+    if (lane > k && lane < n) {
+      const double val = (lane == k + 1) ? beta : 0.0;
+      a[lane * LD + k] = val;
+      a[k * LD + lane] = val;
+    }
+    // v <- v H, H = I - u u^T / h (lane = row of v)
+    if (lane < n) {
+      double w = 0.0;
+      for (int c = k + 1; c < n; ++c) w += v[lane * LD + c] * s.hu[c];
+      w /= h;
+      for (int c = k + 1; c < n; ++c) v[lane * LD + c] -= w * s.hu[c];
+    }
+    __syncwarp();
+  }
+  // ---- tridiagonal: d = diag, e[i] = a[i+1][i] (e[n-1] = 0)
+  if (lane < n) {
+    s.qd[lane] = a[lane * LD + lane];
+    s.qe[lane] = lane + 1 < n ? a[(lane + 1) * LD + lane] : 0.0;
+  }
+  __syncwarp();
+  int info = 0;
+  double f = 0.0, tst1 = 0.0;
+  const double eps = DBL_EPSILON;
+  for (int l = 0; l < n; ++l) {
+    // lane 0 owns the scalar recurrence (d, e in shared memory)
+    int m = l, iter = 0;
+    if (lane == 0) {
+      tst1 = fmax(tst1, fabs(s.qd[l]) + fabs(s.qe[l]));
+      while (m < n - 1 && !(fabs(s.qe[m]) <= eps * tst1)) ++m;
+    }
+    m = __shfl_sync(0xffffffffu, m, 0);
+    while (m > l) {
+      int nrot = 0;
+      if (lane == 0) {
+        ++iter;
+        double g = s.qd[l];
+        double p = (s.qd[l + 1] - g) / (2.0 * s.qe[l]);
+        double r = hypot(p, 1.0);
+        if (p < 0.0) r = -r;
+        s.qd[l] = s.qe[l] / (p + r);
+        s.qd[l + 1] = s.qe[l] * (p + r);
+        const double dl1 = s.qd[l + 1];
+        double hh = g - s.qd[l];
+        for (int i = l + 2; i < n; ++i) s.qd[i] -= hh;
+        f += hh;
+        p = s.qd[m];
+        double c = 1.0, c2 = 1.0, c3 = 1.0, sn = 0.0, s2 = 0.0;
+        const double el1 = s.qe[l + 1];
+        for (int i = m - 1; i >= l; --i) {
+          // r = |(p, e_i)| and its reciprocal from one rsqrt (entries are the
+          // matrix's scale here: no over/underflow guard needed, unlike the
+          // shift above)
+          const double ei = s.qe[i], di = s.qd[i];
+          c3 = c2;
+          c2 = c;
+          s2 = sn;
+          g = c * ei;
+          hh = c * p;
+          const double r2 = fma(p, p, ei * ei);
+          const double rr = rsqrt(r2);
+          s.qe[i + 1] = sn * (r2 * rr);
+          sn = ei * rr;
+          c = p * rr;
+          p = c * di - sn * g;
+          s.qd[i + 1] = hh + sn * (c * g + sn * di);
+          s.qc[nrot] = c;   // rotation of columns (i, i + 1) of v
+          s.qs[nrot] = sn;
+          ++nrot;
+        }
+        p = -sn * s2 * c3 * el1 * s.qe[l] / dl1;
+        s.qe[l] = sn * p;
+        s.qd[l] = c * p;
+        if (fabs(s.qe[l]) <= eps * tst1) m = l;  // converged: leave the loop
+        if (iter > 60) {
+          info = UT_INFO_NO_CONVERGE;
+          m = l;
+        }
+      }
+      nrot = __shfl_sync(0xffffffffu, nrot, 0);
+      const int mm = __shfl_sync(0xffffffffu, m, 0);
+      __syncwarp();
+      if (lane < n) {
+        // apply the step's rotations (i = m0-1 down to l) to row `lane` of v
+        int i = l + nrot - 1;
+        for (int t = 0; t < nrot; ++t, --i) {
+          const double c = s.qc[t], sn = s.qs[t];
+          const double hv = v[lane * LD + i + 1], vi = v[lane * LD + i];
+          v[lane * LD + i + 1] = sn * vi + c * hv;
+          v[lane * LD + i] = c * vi - sn * hv;
+        }
+      }
+      __syncwarp();
+      m = mm;
+    }
+    if (lane == 0) {
+      s.qd[l] += f;
+      s.qe[l] = 0.0;
+    }
+    __syncwarp();
+  }
+  info = __shfl_sync(0xffffffffu, info, 0);
+  if (lane < n)
+    for (int c = 0; c < n; ++c) a[lane * LD + c] = (lane == c) ? s.qd[c] : 0.0;
+  __syncwarp();
+  return info;
+}
+
+#ifndef UT_EIG_QL
+#define UT_EIG_QL 1   // 0: parallel Jacobi only (the round-1 solver)
+#endif
+
+// Eigen-decomposition of the symmetric a (n x n) into (diag a, v), whole CTA
+// calls it.  use_ql: warp 0 runs the Householder + QL solver (if that ever fails
+// to converge, the parallel Jacobi team redoes it from the saved matrix in s.x);
+// otherwise the parallel Jacobi team.  Measured on B200 (tools/probes/
+// solve_speed.py): the generalized CVA problem at B = 32 (C = L^-1 S_b L^-T,
+// rank C - 1, a cluster of null eigenvalues) 296 -> 218 us with QL, while the
+// B = 32 PCA correlation matrix is faster with Jacobi (9 sweeps: ~250 us vs
+// ~300 us for the serial QL chain) and the 6 x 6 low-rank problem is a tie.
+// Returns an info code (uniform across the CTA).
+__device__ int sym_eig(Smem& s, double* a, double* v, int n, bool use_ql) {
+  const int tid = threadIdx.x;
+  if (UT_EIG_QL && use_ql) {
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      s.x[i * LD + j] = a[i * LD + j];
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const int code = ql_warp(s, a, v, n);
+      if (tid == 0) s.flag = code;
+    }
+    __syncthreads();
+    if (s.flag == 0) return 0;
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      a[i * LD + j] = s.x[i * LD + j];
+    }
+    __syncthreads();
+  }
+  if (tid < kTeam) {
+    const int code = jacobi_team<kTeam>(s, a, v, n);
+    if (tid == 0) s.flag = code;
+  }
+  __syncthreads();
+  return s.flag;
+}
+
 // Cholesky of m (lower, in place) by warp 0; false if a pivot is not > 0.
 __device__ bool chol_warp(double* m, int n) {
   const int lane = threadIdx.x & 31;
@@ -412,8 +605,7 @@ __device__ int solve_full(Smem& s, int n, bool generalized, double ridge, bool c
     if (!s.flag) {
       if (i < n && j < n) s.a[i * LD + j] = 0.5 * (s.x[i * LD + j] + s.x[j * LD + i]);
       __syncthreads();
-      if (tid < kTeam) jacobi_team<kTeam>(s, s.a, s.v, n);
-      __syncthreads();
+      sym_eig(s, s.a, s.v, n, false);
       sort_desc(s, s.a, n);
       if (tid < n) aux[tid] = s.a[s.order[tid] * LD + s.order[tid]];
       return UT_INFO_NOT_PD;
@@ -433,12 +625,7 @@ __device__ int solve_full(Smem& s, int n, bool generalized, double ridge, bool c
     if (i < n && j < n) s.a[i * LD + j] = s.x[i * LD + j];
     __syncthreads();
   }
-  if (tid < kTeam) {
-    const int code = jacobi_team<kTeam>(s, s.a, s.v, n);
-    if (tid == 0) s.flag = code;
-  }
-  __syncthreads();
-  const int info = s.flag;
+  const int info = sym_eig(s, s.a, s.v, n, generalized);
   sort_desc(s, s.a, n);
   if (generalized) {
     // V = L^-T U (eigen.py:112)

@@ -325,14 +325,19 @@ class TestProjectStack:
             b.project_stack(raw, model(np.eye(6), provenance={"normalized_input": True}))
 
     def test_plane_variance_follows_eigenvalue_order(self):
-        """:309-321 -- the training multiset laid out as an image"""
+        """:309-321 -- the training multiset laid out as an image: a plane's
+        variance is (1 + lambda) / N.  The 3 = C - 1 significant components must
+        come in order; the two null-space components (lambda ~ 1e-14, vectors
+        numerically arbitrary -- SURVEY Appendix A) have equal variance up to
+        the fp32 storage of the planes (1e-6 here, not the reference's fp64 1e-9)."""
         rng = np.random.default_rng(16)
         v = rng.integers(0, 255, size=(5, 64)).astype(np.float64)
         labels = np.repeat(np.arange(4), 16)
         m = b.fit_cva(dm(v, labels))
         planes = b.project_stack(stack_of(v.reshape(5, 8, 8)), m)
-        var = [values_of(p).var() for p in planes]
-        assert (np.diff(var) <= 1e-9 * max(var)).all()
+        var = np.array([values_of(p).var() for p in planes])
+        assert (np.diff(var[:3]) <= 1e-9 * var.max()).all()
+        assert (np.diff(var) <= 1e-6 * var.max()).all()
 
 
 class TestModelSerialization:
