@@ -234,3 +234,24 @@ def test_pipeline_fit_model_and_render_planes_end_to_end(tmp_path):
     for p, plane in zip(res.plane_paths, planes):
         img = cv2.imread(str(p), cv2.IMREAD_UNCHANGED)
         assert np.array_equal(img, np.asarray(b.rescale_full(plane)))
+
+
+def test_lda_at_bench_scale_vs_oracle():
+    """fit_lda on a device design matrix of the cfg 4 shape (B = 32, two classes,
+    20,000 points each) against the oracle's standardize + CVA (projection.py:240-260)."""
+    from paper_1612_06457_b200 import synthetic
+
+    cfg = synthetic.scaled(synthetic.CONFIGS["cfg4"], 2048, 2048, per_class=20_000)
+    scene = synthetic.make_scene(cfg)
+    stack = synthetic.generate(scene)
+    keep = scene.labels < 2
+    xy = torch.from_numpy(np.stack([scene.xs[keep], scene.ys[keep]], 1).astype(np.int32)).cuda()
+    values, bad = b.annotations.gather(stack, xy, int(keep.sum()))
+    assert int(bad.item()) == -1
+    labels = scene.labels[keep].astype(np.intp)
+    dm = b.DesignMatrix(values, labels, ("c0", "c1"))
+    m = b.fit_lda(dm, k=1)
+    ref = oracle.fit_lda(values.cpu().numpy(), labels, k=1)
+    assert rel_close(m.mean, ref["mean"], 1e-9) and rel_close(m.std, ref["std"], 1e-9)
+    assert rel_close(m.eigenvalues, ref["eigenvalues"], 1e-9)
+    assert rel_close(align_signs(m.coefficients, ref["coefficients"]), ref["coefficients"], 1e-6)
