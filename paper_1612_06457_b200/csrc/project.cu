@@ -529,7 +529,10 @@ project_dmma_kernel(ProjParams p) {
       double c0[kDmmaGroups], c1[kDmmaGroups];
 #pragma unroll
       for (int g = 0; g < kDmmaGroups; ++g) c0[g] = c1[g] = 0.0;
-      // B fragment: B[k = lane%4][n = lane/4] = x[band 4q + lane%4][pixel n]
+      // B fragment of group g: B[k = lane%4][n = lane/4] = x[band 4q + lane%4][pixel
+      // wp0 + G n + g] (G = kDmmaGroups): a lane's G samples of a band are
+      // consecutive, one vector load (16 B for fp32) instead of G scalar loads, and
+      // its G scores of a component come out consecutive as well
       const int bk = lane & 3, bn = lane >> 2;
       __syncwarp();  // mma.sync.aligned: the whole warp, converged
 #pragma unroll
@@ -541,32 +544,48 @@ project_dmma_kernel(ProjParams p) {
           // zero, so they add nothing -- a NaN / Inf there is a NaN / Inf of
           // this pixel's band 0, which its own term propagates as well and the
           // nonfinite guard reports
-          const T* row = stage + (size_t)(b < B ? b : 0) * PS + wp0 + bn;
+          const T* row = stage + (size_t)(b < B ? b : 0) * PS + wp0 + kDmmaGroups * bn;
+          T xs[kDmmaGroups];
+#pragma unroll
+          for (int v = 0; v < (int)(kDmmaGroups * sizeof(T)) / 16; ++v)
+            reinterpret_cast<uint4*>(xs)[v] = reinterpret_cast<const uint4*>(row)[v];
           double x[kDmmaGroups];
 #pragma unroll
           for (int g = 0; g < kDmmaGroups; ++g)
             // the first UT_DMMA_F2F groups widen on the conversion pipe (F2F),
             // the rest with ALU bit operations
-            x[g] = (g < UT_DMMA_F2F) ? to_f64(row[8 * g]) : widen_f64(row[8 * g]);
+            x[g] = (g < UT_DMMA_F2F) ? to_f64(xs[g]) : widen_f64(xs[g]);
 #pragma unroll
           for (int g = 0; g < kDmmaGroups; ++g) dmma_884(c0[g], c1[g], afrag[q], x[g]);
         }
       }
-      // C[m = lane/4][n = 2 (lane%4) + {0,1}] -> scores of component m
+      // C[m = lane/4][n = 2 (lane%4) + h], h = 0, 1 (c0 / c1) -> scores of component m
+      // at pixels wp0 + G n + g, g = 0 .. G - 1 (consecutive)
       if (am < KG) {
-        const int cn = 2 * (lane & 3);
 #pragma unroll
-        for (int g = 0; g < kDmmaGroups; ++g) {
-          const int lp = wp0 + 8 * g + cn;
-          if (lp + 2 <= npx) {
-            float o[2] = {(float)(c0[g] + bias), (float)(c1[g] + bias)};
+        for (int h = 0; h < 2; ++h) {
+          const int lp = wp0 + kDmmaGroups * (2 * (lane & 3) + h);
+          float o[kDmmaGroups];
 #pragma unroll
-            for (int v = 0; v < 2; ++v) {
-              lmn = fminf(lmn, o[v]);
-              lmx = fmaxf(lmx, o[v]);
-              chk = nan_guard(chk, o[v]);
+          for (int g = 0; g < kDmmaGroups; ++g) o[g] = (float)((h ? c1[g] : c0[g]) + bias);
+          float* dst = p.scores + (int64_t)(p.k0 + am) * p.npix + p0 + lp;
+          if (lp + kDmmaGroups <= npx) {
+#pragma unroll
+            for (int g = 0; g < kDmmaGroups; ++g) {
+              lmn = fminf(lmn, o[g]);
+              lmx = fmaxf(lmx, o[g]);
+              chk = nan_guard(chk, o[g]);
             }
-            store_scores<2>(p.scores + (int64_t)(p.k0 + am) * p.npix + p0 + lp, o);
+            store_scores<kDmmaGroups>(dst, o);
+          } else {
+#pragma unroll
+            for (int g = 0; g < kDmmaGroups; ++g)
+              if (lp + g < npx) {
+                lmn = fminf(lmn, o[g]);
+                lmx = fmaxf(lmx, o[g]);
+                chk = nan_guard(chk, o[g]);
+                dst[g] = o[g];
+              }
           }
         }
       }
