@@ -133,3 +133,20 @@ def test_sharded_local_record_does_not_alias_gather_output():
         assert hi <= out.data_ptr() or lo >= out.data_ptr() + out.numel() * 8
     for fit in (CvaDevice(8, 3, "cpu"), PcaDevice(8, "cpu")):
         assert fit.local_moments().data_ptr() == fit.moments.data_ptr()
+
+
+def test_render_batch_sized_to_free_memory(monkeypatch):
+    """render_planes projects up to 32 components per pass only when
+    their fp32 planes and codes fit in half the free HBM (the reference batches
+    8 to bound memory); otherwise fewer, never 0."""
+    import types
+
+    import torch
+
+    from paper_1612_06457_b200 import pipeline
+
+    ds = types.SimpleNamespace(height=16384, width=16384, planes=types.SimpleNamespace(device="cuda:0"))
+    per_comp = 16384 * 16384 * (4 + 2 * 1)           # one spec, 16-bit codes bound
+    for free, want in ((10**12, 32), (20 * per_comp, 10), (per_comp, 1), (0, 1)):
+        monkeypatch.setattr(torch.cuda, "mem_get_info", lambda device=None, f=free: (f, 2 * f + 1))
+        assert pipeline._render_batch(ds, 1) == want, (free, want)
