@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--rows", type=int, default=None, help="override image height (profiling)")
     ap.add_argument("--precision", default=None, choices=[None, "fp32", "fp64"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=7)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-stream-e2e", action="store_true", help="serial e2e only")
     ap.add_argument("--no-cpu", action="store_true")
