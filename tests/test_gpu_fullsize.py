@@ -186,3 +186,32 @@ def test_cfg3_fit_full_size_vs_oracle():
     assert eig_close(h["evals"][:cfg.k], ref["eigenvalues"], float(np.abs(full[0]).max()))
     assert rel_close(align_signs(h["evecs"][:, :cfg.k], ref["coefficients"]),
                      ref["coefficients"], VEC_TOL)
+
+
+def test_cfg4_rerun_bit_identical_and_scale_invariant(cfg4_cube):
+    """Size-independent properties at the bench size: (1) the full CVA step is
+    bit-identical run to run (fixed reduction orders, no float atomics); (2) CVA
+    is invariant to a global rescaling of the cube: with 2x the data the scatter
+    matrices scale by 4, the W'-orthonormal canonical vectors by 1/2, and the
+    score planes are unchanged -- to the 1e-6-of-range parity bar (fp32 planes),
+    codes within one level."""
+    cfg, scene, stack, host = cfg4_cube
+    pipe = ut.CvaPipeline(stack, scene.xs, scene.ys, scene.labels, k=cfg.k)
+    codes1 = pipe.run().clone()
+    scores1 = pipe.scores.clone()
+    pipe.run()
+    torch.cuda.synchronize()
+    assert torch.equal(pipe.codes, codes1)
+    assert torch.equal(pipe.scores, scores1)
+    del pipe
+    doubled = ut.DeviceStack(stack.bands, stack.planes * 2, stack.bit_depth, True)
+    pipe2 = ut.CvaPipeline(doubled, scene.xs, scene.ys, scene.labels, k=cfg.k)
+    codes2 = pipe2.run()
+    torch.cuda.synchronize()
+    for j in range(cfg.k):
+        s1, s2 = scores1[j], pipe2.scores[j]
+        rng = float(s1.max() - s1.min())
+        assert float((s1 - s2).abs().max()) <= 1e-6 * rng, j
+        assert int((codes1[j].int() - codes2[j].int()).abs().max()) <= 1, j
+    del pipe2, doubled, scores1, codes1
+    torch.cuda.empty_cache()
