@@ -20,6 +20,13 @@
 
 #include "common.cuh"
 
+#ifndef UT_PROD_LANES   // project_tma_kernel: the producer warp's lanes share the band copies
+#define UT_PROD_LANES 1     // (cfg 3: K4 0.531 -> 0.443 ms; 0 = one lane issues them all)
+#endif
+#ifndef UT_DMMA_PROD_LANES  // project_dmma_kernel: its two producer warps each issue from one
+#define UT_DMMA_PROD_LANES 0  // lane (all lanes measured 0.4% slower on the cfg 4 step)
+#endif
+
 namespace ut {
 namespace {
 
@@ -382,23 +389,22 @@ project_tma_kernel(ProjParams p, int P, int R) {
   }
   const int64_t ntiles = (p.npix + P - 1) / P;
   if (warp == CONS / 32) {
-    // producer
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      int i = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-        const int st = i % kTmaStages;
-        const uint32_t ph = (uint32_t)(i / kTmaStages) & 1u;
-        if (i >= kTmaStages) mbar_wait(&empty[st], ph ^ 1u);
-        const int64_t p0 = t * P;
-        const int64_t npx = (p.npix - p0) < P ? (p.npix - p0) : P;
-        const uint32_t bytes = (uint32_t)(npx * sizeof(T));
-        mbar_expect_tx(&full[st], bytes * (uint32_t)B);
-        T* dst = stages + (size_t)st * P * B;
-        const T* src = static_cast<const T*>(p.data) + p0;
-        for (int b = 0; b < B; ++b)
-          bulk_g2s(dst + (size_t)b * P, src + (int64_t)b * p.bs, bytes, &full[st], pol);
-      }
+    // producer warp: lane 0 arms the stage, every lane issues some band copies
+    const uint64_t pol = policy_evict_first();
+    int i = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int st = i % kTmaStages;
+      const uint32_t ph = (uint32_t)(i / kTmaStages) & 1u;
+      if (i >= kTmaStages) mbar_wait(&empty[st], ph ^ 1u);
+      const int64_t p0 = t * P;
+      const int64_t npx = (p.npix - p0) < P ? (p.npix - p0) : P;
+      const uint32_t bytes = (uint32_t)(npx * sizeof(T));
+      if (lane == 0) mbar_expect_tx(&full[st], bytes * (uint32_t)B);
+      __syncwarp();
+      T* dst = stages + (size_t)st * P * B;
+      const T* src = static_cast<const T*>(p.data) + p0;
+      for (int b = UT_PROD_LANES ? lane : (lane == 0 ? 0 : B); b < B; b += UT_PROD_LANES ? 32 : 1)
+        bulk_g2s(dst + (size_t)b * P, src + (int64_t)b * p.bs, bytes, &full[st], pol);
     }
   } else {
     int i = 0;
@@ -487,6 +493,27 @@ project_dmma_kernel(ProjParams p) {
   if (warp >= kDmmaCons / 32) {
     // producers: warp pw issues the rows of bands pw, pw + kDmmaProd, ...
     const int pw = warp - kDmmaCons / 32;
+#if UT_DMMA_PROD_LANES   // every lane of the producer warp issues some of the band copies
+    {
+      const uint64_t pol = policy_evict_first();
+      const int nb = B > pw ? (B - 1 - pw) / kDmmaProd + 1 : 0;
+      int i = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int st = i % kTmaStages;
+        const uint32_t ph = (uint32_t)(i / kTmaStages) & 1u;
+        if (i >= kTmaStages) mbar_wait(&empty[st], ph ^ 1u);
+        const int64_t p0 = t * kDmmaP;
+        const int64_t npx = (p.npix - p0) < kDmmaP ? (p.npix - p0) : kDmmaP;
+        const uint32_t bytes = (uint32_t)(npx * sizeof(T));
+        if (lane == 0) mbar_expect_tx(&full[st], bytes * (uint32_t)nb);
+        __syncwarp();
+        T* dst = stages + (size_t)st * B * PS;
+        const T* src = static_cast<const T*>(p.data) + p0;
+        for (int b = pw + kDmmaProd * lane; b < B; b += kDmmaProd * 32)
+          bulk_g2s(dst + (size_t)b * PS, src + (int64_t)b * p.bs, bytes, &full[st], pol);
+      }
+    }
+#else
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       const int nb = B > pw ? (B - 1 - pw) / kDmmaProd + 1 : 0;
@@ -505,6 +532,7 @@ project_dmma_kernel(ProjParams p) {
           bulk_g2s(dst + (size_t)b * PS, src + (int64_t)b * p.bs, bytes, &full[st], pol);
       }
     }
+#endif
   } else {
     // A fragments: A[m = lane/4][k = lane%4] = w[band 4q + lane%4][comp lane/4]
     const int am = lane >> 2, ak = lane & 3;
