@@ -20,6 +20,13 @@
 
 #include "common.cuh"
 
+#ifndef UT_RD_PROD_LANES   // region_dmma_kernel: lanes share the band copies (0 = one lane)
+#define UT_RD_PROD_LANES 1
+#endif
+#ifndef UT_IM_PROD_LANES   // region_imma_kernel: lanes of each producer warp share its copies
+#define UT_IM_PROD_LANES 1
+#endif
+
 namespace ut {
 namespace {
 
@@ -346,22 +353,22 @@ region_dmma_kernel(RdParams r) {
 #pragma unroll
   for (int g = 0; g < NG; ++g) dsum[g] = 0.0;
   if (warp == kRdCons / 32) {
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      int i = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-        const int st = i % kRdStages;
-        const uint32_t ph = (uint32_t)(i / kRdStages) & 1u;
-        if (i >= kRdStages) mbar_wait(&empty[st], ph ^ 1u);
-        const int64_t p0 = t * kRdP;
-        const int64_t npx = (r.npix - p0) < kRdP ? (r.npix - p0) : kRdP;
-        const uint32_t bytes = (uint32_t)(npx * sizeof(T));
-        mbar_expect_tx(&full[st], bytes * (uint32_t)B);
-        T* dst = stages + (size_t)st * B * PS;
-        const T* src = static_cast<const T*>(r.data) + p0;
-        for (int b = 0; b < B; ++b)
-          bulk_g2s(dst + (size_t)b * PS, src + (int64_t)b * r.bs, bytes, &full[st], pol);
-      }
+    // producer warp: lane 0 arms the stage, the lanes share the band copies
+    const uint64_t pol = policy_evict_first();
+    int i = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int st = i % kRdStages;
+      const uint32_t ph = (uint32_t)(i / kRdStages) & 1u;
+      if (i >= kRdStages) mbar_wait(&empty[st], ph ^ 1u);
+      const int64_t p0 = t * kRdP;
+      const int64_t npx = (r.npix - p0) < kRdP ? (r.npix - p0) : kRdP;
+      const uint32_t bytes = (uint32_t)(npx * sizeof(T));
+      if (lane == 0) mbar_expect_tx(&full[st], bytes * (uint32_t)B);
+      __syncwarp();
+      T* dst = stages + (size_t)st * B * PS;
+      const T* src = static_cast<const T*>(r.data) + p0;
+      for (int b = UT_RD_PROD_LANES ? lane : (lane == 0 ? 0 : B); b < B; b += UT_RD_PROD_LANES ? 32 : 1)
+        bulk_g2s(dst + (size_t)b * PS, src + (int64_t)b * r.bs, bytes, &full[st], pol);
     }
   } else {
     const int fb = lane >> 2, fp = lane & 3;  // fragment: band 8g + fb, pixel fp of the quad
@@ -680,6 +687,25 @@ region_imma_kernel(ImParams r) {
 
   if (warp < kImProd) {
     // ------------------------------------------------- producers (bands p, p+4, ...)
+#if UT_IM_PROD_LANES   // the producer warps' lanes share the band copies
+    {
+      const uint64_t pol = policy_evict_first();
+      const int nb = B > warp ? (B - 1 - warp) / kImProd + 1 : 0;
+      for (int i = 0; i < nloc; ++i) {
+        const int st = i % kImStagesIn;
+        if (i >= kImStagesIn) im_wait(&in_empty[st], ((i / kImStagesIn) - 1) & 1);
+        const int64_t p0 = ((int64_t)blockIdx.x + (int64_t)i * r.G) * kImP;
+        const int64_t npx = (r.npix - p0) < kImP ? (r.npix - p0) : kImP;
+        const uint32_t bytes = (uint32_t)(npx * sizeof(T));
+        if (lane == 0) mbar_expect_tx(&in_full[st], bytes * (uint32_t)nb);
+        __syncwarp();
+        T* dst = in + (size_t)st * kMaxBands * PS;
+        const T* src = static_cast<const T*>(r.data) + p0;
+        for (int b = warp + kImProd * lane; b < B; b += kImProd * 32)
+          bulk_g2s(dst + (size_t)b * PS, src + (int64_t)b * r.bs, bytes, &in_full[st], pol);
+      }
+    }
+#else
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       const int nb = B > warp ? (B - 1 - warp) / kImProd + 1 : 0;
@@ -696,6 +722,7 @@ region_imma_kernel(ImParams r) {
           bulk_g2s(dst + (size_t)b * PS, src + (int64_t)b * r.bs, bytes, &in_full[st], pol);
       }
     }
+#endif
   } else if (warp == kImProd) {
     // -------------------------------------------------------------- MMA issue
     if (lane == 0) {
