@@ -10,12 +10,15 @@
 // pipeline; the chunk's coordinates are staged first so all sample loads are
 // independent) or read from a B x n design matrix -- as deviations from the
 // class pivot (the first point of the class), with a constant-1 row appended,
-// and accumulates the upper triangle of [d;1][d;1]^T per class: one Gram holds
-// the count, the shifted sums and the shifted scatter.  A merge kernel (one
-// warp per output entry, lanes over ranges, fixed shuffle tree) sums the G
-// partials and finalizes mean = pivot + s/n, M2 = S - s s^T/n.  Centring on a
-// pivot keeps the one-pass form as accurate as the reference's two-pass form;
-// every reduction order is fixed, so results are bit-identical run to run.
+// and accumulates the upper triangle of [d;1][d;1]^T per class on the fp64
+// tensor cores (mma.sync.m8n8k4.f64; each warp owns up to two 8x8 blocks of the
+// upper triangle): one Gram holds the count, the shifted sums and the shifted
+// scatter.  A CTA writes the records of the classes it saw, contiguously, plus
+// its class mask; the merge kernel (one thread per Gram entry, ranges in
+// ascending order) sums the partials of the ranges that saw the class and
+// finalizes mean = pivot + s/n, M2 = S - s s^T/n.  Centring on a pivot keeps the
+// one-pass form as accurate as the reference's two-pass form; every reduction
+// order is fixed, so results are bit-identical run to run.
 #include "common.cuh"
 
 namespace ut {
@@ -34,10 +37,19 @@ constexpr int kMinPerCta = UT_K1_MINPER;  // points per CTA at least (multiple o
 constexpr int kSmallG = UT_K1_SMALL_G;  // up to this many 128-point CTAs, no 2-chunk minimum
 constexpr int kMaxClasses = 16;  // per launch; more classes -> several launches
 constexpr int kRows = kMaxBands + 1;                    // bands + ones row
-constexpr int kMaxEnt = kRows * (kRows + 1) / 2;        // 561
-constexpr int kTileLd = kChunk + 1;
+constexpr int kTileLd = kChunk + 4;   // row stride = 4 mod 16 doubles: a fragment load (8 rows x 4 points) is conflict-free
+constexpr int kWarps = kThreads / 32;
 
 __host__ __device__ inline int ent_count(int b) { return (b + 1) * (b + 2) / 2; }
+__host__ __device__ inline int row_groups(int b) { return (b + 1 + 7) / 8; }   // 8-row groups incl. the ones row
+// upper-triangle entry (i <= j) of the (B+1) x (B+1) Gram, R = B + 1
+__host__ __device__ inline int ent_index(int i, int j, int R) { return i * R - i * (i - 1) / 2 + (j - i); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
 
 // ------------------------------------------------------------------ gather
 template <typename T>
@@ -82,6 +94,40 @@ struct MatrixSrc {
   __device__ __forceinline__ double at_global(int b, int64_t j) const { return values[b * ld + j]; }
 };
 
+// One gathered sample: read-only path, no L1 allocation, 64-byte L2 fetch hint --
+// every sample of a training pixel sits in another band plane, so nothing near it
+// is used (cfg 4 fit: K1 118 -> 112 us in A/B runs).
+#ifndef UT_K1_L2HINT
+#define UT_K1_L2HINT 1
+#endif
+template <typename T>
+__device__ __forceinline__ T ld_gather(const T* p) {
+#if UT_K1_L2HINT
+  T out;
+  if constexpr (sizeof(T) == 1) {
+    uint16_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.u8 %0, [%1];" : "=h"(v) : "l"(p));
+    const uint8_t w = (uint8_t)v;
+    memcpy(&out, &w, 1);
+  } else if constexpr (sizeof(T) == 2) {
+    uint16_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.b16 %0, [%1];" : "=h"(v) : "l"(p));
+    memcpy(&out, &v, 2);
+  } else if constexpr (sizeof(T) == 4) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    memcpy(&out, &v, 4);
+  } else {
+    unsigned long long v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.b64 %0, [%1];" : "=l"(v) : "l"(p));
+    memcpy(&out, &v, 8);
+  }
+  return out;
+#else
+  return *p;
+#endif
+}
+
 template <typename T>
 struct CubeSrc {
   const T* data;
@@ -90,7 +136,7 @@ struct CubeSrc {
   using Coord = int2;  // (x, local y)
   using Raw = T;
   __device__ __forceinline__ Raw raw(int b, Coord c) const {
-    return data[b * bs + (int64_t)c.y * rs + c.x];
+    return ld_gather(data + (b * bs + (int64_t)c.y * rs + c.x));
   }
   __device__ __forceinline__ static double widen(Raw v) { return to_f64(v); }
   __device__ __forceinline__ Coord coord(int64_t j) const {
@@ -134,22 +180,20 @@ struct Layout {
 __host__ __device__ inline int rec_len(int b) { return 1 + b + b * b; }
 
 // Shared memory, sized for the launch's B and C (dynamic):
-//   tile[(B+1) x kTileLd] | acc[C x E] | pivot[C x B] | lbl[kChunk] | mask | pi, pj[E]
+//   tile[8 NG x kTileLd] | acc[C x E] | pivot[C x B] | lbl[kChunk] | mask
+// (NG = row groups of 8; the rows past the ones row stay zero)
 struct Smem {
   double* tile;
   double* acc;
   double* pivot;
   int* lbl;
   unsigned* mask_p;
-  unsigned char* pi;
-  unsigned char* pj;
 };
 
 __host__ __device__ inline size_t smem_bytes(int b, int c) {
   const int E = ent_count(b);
-  size_t off = sizeof(double) * ((size_t)(b + 1) * kTileLd + (size_t)c * E + (size_t)c * b);
+  size_t off = sizeof(double) * ((size_t)8 * row_groups(b) * kTileLd + (size_t)c * E + (size_t)c * b);
   off += sizeof(int) * kChunk + 16;
-  off += 2 * (size_t)E;
   return (off + 15) & ~(size_t)15;
 }
 
@@ -158,13 +202,11 @@ __device__ inline Smem carve(unsigned char* raw, int b, int c) {
   Smem s;
   double* d = reinterpret_cast<double*>(raw);
   s.tile = d;
-  s.acc = d + (size_t)(b + 1) * kTileLd;
+  s.acc = d + (size_t)8 * row_groups(b) * kTileLd;
   s.pivot = s.acc + (size_t)c * E;
   int* ip = reinterpret_cast<int*>(s.pivot + (size_t)c * b);
   s.lbl = ip;
   s.mask_p = reinterpret_cast<unsigned*>(ip + kChunk);
-  s.pi = reinterpret_cast<unsigned char*>(s.mask_p + 4);
-  s.pj = s.pi + E;
   return s;
 }
 
@@ -187,11 +229,13 @@ pivot_kernel(const int32_t* __restrict__ cls, int64_t n, int c0, int classes, in
     pivots[threadIdx.x] = first[threadIdx.x] == 0x7fffffff ? -1 : first[threadIdx.x];
 }
 
-// Per-range Gram of [x - pivot_c ; 1] per class -> part[c][e][g] (raw sums).
+// Per-range Gram of [x - pivot_c ; 1] per class -> part[g][c][e] (raw sums) for
+// the classes range g saw, cmask[g] = those classes.
 template <typename Src>
 __global__ void __launch_bounds__(kThreads)
 moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restrict__ pivots,
-               Layout L, double* __restrict__ part, unsigned long long* first_bad) {
+               Layout L, double* __restrict__ part, uint32_t* __restrict__ cmask,
+               double* __restrict__ pivval, unsigned long long* first_bad) {
   extern __shared__ __align__(16) unsigned char raw[];
   const Smem s = carve(raw, L.bands, L.classes);
   const int tid = threadIdx.x;
@@ -207,6 +251,7 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restri
   constexpr int kPer = kMaxBands / (kThreads / kChunk);  // 16 bands per thread
   const int sp = tid % kChunk, sb = tid / kChunk;
   typename Src::Raw nv[kPer];
+  unsigned seen = 0u;              // classes of the chunks so far
   int nl = -1;                     // label of the chunk in nv
   typename Src::Coord ncc{};       // coordinates two chunks ahead
   int nnl = -1;
@@ -241,22 +286,19 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restri
     load_samples(j0);
     if (j0 + kChunk < j1) load_coord(j0 + kChunk);
   }
-  for (int i = tid; i < R; i += blockDim.x) {
-    const int base = i * R - i * (i - 1) / 2;
-    for (int j = i; j < R; ++j) {
-      s.pi[base + j - i] = (unsigned char)i;
-      s.pj[base + j - i] = (unsigned char)j;
-    }
-  }
+  const int NG = row_groups(B), NB = NG * (NG + 1) / 2;
+  const int lane = tid & 31, warp = tid >> 5, fb = lane >> 2, fp = lane & 3;
+  for (int e = tid; e < 8 * NG * kTileLd; e += blockDim.x) s.tile[e] = 0.0;
   for (int e = tid; e < C * E; e += blockDim.x) s.acc[e] = 0.0;
   for (int e = tid; e < C * B; e += blockDim.x) {
     const int c = e / B, b = e - c * B;
     const int pj = pivots[c];
-    s.pivot[e] = (pj >= 0 && src.valid(pj)) ? src.at_global(b, pj) : 0.0;
+    const double v = (pj >= 0 && src.valid(pj)) ? src.at_global(b, pj) : 0.0;
+    s.pivot[e] = v;
+    if (blockIdx.x == 0) pivval[e] = v;   // for the merge
   }
   __syncthreads();
   for (int64_t q0 = j0; q0 < j1; q0 += kChunk) {
-    const int count = (int)((j1 - q0) < kChunk ? (j1 - q0) : kChunk);
     if (tid == 0) *s.mask_p = 0u;
     __syncthreads();
     // deviations from the class pivot; row B is the constant 1 (0 for padding)
@@ -275,80 +317,128 @@ moments_kernel(Src src, const int32_t* __restrict__ cls, const int32_t* __restri
     if (q0 + kChunk < j1) load_samples(q0 + kChunk);
     if (q0 + 2 * kChunk < j1) load_coord(q0 + 2 * kChunk);
     const unsigned mask = *s.mask_p;
-    if (mask != 0u && (mask & (mask - 1u)) == 0u) {
-      // one class in this chunk (class-sorted points): branch-free loop;
-      // padding / foreign points are zero rows and add nothing
-      const int c = __ffs(mask) - 1;
-      for (int e = tid; e < E; e += blockDim.x) {
-        const double* ri = s.tile + s.pi[e] * kTileLd;
-        const double* rj = s.tile + s.pj[e] * kTileLd;
-        double a = s.acc[c * E + e];
-#pragma unroll 8
-        for (int p = 0; p < kChunk; ++p) a = fma(ri[p], rj[p], a);
-        s.acc[c * E + e] = a;
-      }
-    } else if (mask != 0u) {
-      // mixed chunk: one class run at a time
-      for (int e = tid; e < E; e += blockDim.x) {
-        const double* ri = s.tile + s.pi[e] * kTileLd;
-        const double* rj = s.tile + s.pj[e] * kTileLd;
-        int cur = -1;
-        double a = 0.0;
-        for (int p = 0; p < count; ++p) {
-          const int c = s.lbl[p];
-          if (c < 0) continue;
-          if (c != cur) {
-            if (cur >= 0) s.acc[cur * E + e] = a;
-            cur = c;
-            a = s.acc[c * E + e];
+    seen |= mask;
+    // Gram of the chunk on the fp64 tensor cores.  Warp w owns the upper 8x8
+    // blocks w, w + 8 (< NB); a lane's A element is tile[8 bi + fb][k + fp], its
+    // B element tile[8 bj + fb][k + fp]; two accumulator pairs over alternate
+    // 4-point steps.  One class in the chunk (class-sorted points): one pass,
+    // padding / foreign points are zero rows.  Mixed chunk: one pass per class
+    // present, the B element masked to the class's points.
+    const bool single = (mask & (mask - 1u)) == 0u;
+    for (unsigned rest = mask; rest != 0u; rest &= rest - 1u) {
+      const int c = __ffs(rest) - 1;
+      for (int q = warp; q < NB; q += kWarps) {   // warp-uniform
+        int bi = 0, rem = q;
+        while (rem >= NG - bi) { rem -= NG - bi; ++bi; }
+        const int bj = bi + rem;
+        const double* ra = s.tile + (8 * bi + fb) * kTileLd + fp;
+        const double* rb = s.tile + (8 * bj + fb) * kTileLd + fp;
+        double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+        if (single) {
+#pragma unroll 4
+          for (int k = 0; k < kChunk; k += 8) {
+            dmma(c0, c1, ra[k], rb[k]);
+            dmma(d0, d1, ra[k + 4], rb[k + 4]);
           }
-          a = fma(ri[p], rj[p], a);
+        } else {
+#pragma unroll 4
+          for (int k = 0; k < kChunk; k += 8) {
+            const double b0 = s.lbl[k + fp] == c ? rb[k] : 0.0;
+            const double b1 = s.lbl[k + 4 + fp] == c ? rb[k + 4] : 0.0;
+            dmma(c0, c1, ra[k], b0);
+            dmma(d0, d1, ra[k + 4], b1);
+          }
         }
-        if (cur >= 0) s.acc[cur * E + e] = a;
+        c0 += d0;
+        c1 += d1;
+        // the lane holds Gram[8 bi + fb][8 bj + 2 fp, + 1]; each upper entry has one owner
+        const int i = 8 * bi + fb, j = 8 * bj + 2 * fp;
+        if (i < R && j < R && i <= j) s.acc[c * E + ent_index(i, j, R)] += c0;
+        if (i < R && j + 1 < R && i <= j + 1) s.acc[c * E + ent_index(i, j + 1, R)] += c1;
       }
     }
     __syncthreads();
   }
-  const int G = L.G;
-  for (int e = tid; e < C * E; e += blockDim.x) part[(size_t)e * G + blockIdx.x] = s.acc[e];
+  // the records of the classes this range saw, contiguous per range
+  double* rec = part + (size_t)blockIdx.x * C * E;
+  for (int e = tid; e < C * E; e += blockDim.x)
+    if ((seen >> (e / E)) & 1u) rec[e] = s.acc[e];
+  if (tid == 0) cmask[blockIdx.x] = seen;
 }
 
-// One warp per output entry (c, f): sums the G range partials (fixed shuffle
-// tree) and finalizes count / mean = pivot + s/n / M2 = S - s s^T / n.
-template <typename Src>
-__global__ void __launch_bounds__(256)
-merge_kernel(Src src, const double* __restrict__ part, const int32_t* __restrict__ pivots,
-             Layout L, double* __restrict__ moments) {
-  const int B = L.bands, G = L.G;
+// CTA (x, c): threads 0..127 own Gram entries e = 128 x + tid of class c, threads
+// 128..128+B the ones-column entries (i, B) every finalization needs.  Each sums
+// its entry over the ranges that saw the class, in ascending range order, and the
+// CTA finalizes count / mean = pivot + s/n / M2 = S - s s^T / n for its entries.
+constexpr int kMergeEnt = 128;
+constexpr int kMergeThreads = kMergeEnt + 64;
+static_assert(kRows <= 64, "ones-column threads");
+
+__global__ void __launch_bounds__(kMergeThreads)
+merge_kernel(const double* __restrict__ part, const uint32_t* __restrict__ cmask,
+             const double* __restrict__ pivval, Layout L, double* __restrict__ moments) {
+  __shared__ int act[kMaxG];
+  __shared__ int nact_sh;
+  __shared__ double ones[kRows];
+  const int B = L.bands, G = L.G, C = L.classes;
   const int R = B + 1, E = ent_count(B), len = rec_len(B);
-  const int lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= (int64_t)L.classes * len) return;
-  const int c = (int)(w / len), f = (int)(w - (int64_t)c * len);
-  auto sum = [&](int i, int j) {  // Gram entry (i, j) of class c, summed over ranges
-    if (i > j) { const int t = i; i = j; j = t; }
-    const int e = i * R - i * (i - 1) / 2 + (j - i);
-    const double* p = part + ((size_t)c * E + e) * G;
-    double a = 0.0;
-    for (int g = lane; g < G; g += 32) a += p[g];
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    return a;
-  };
-  const double n = sum(B, B);
-  double v = 0.0;
-  if (n > 0.0) {
-    if (f == 0) {
-      v = n;
-    } else if (f <= B) {
-      const int b = f - 1;
-      const int pj = pivots[c];
-      v = ((pj >= 0 && src.valid(pj)) ? src.at_global(b, pj) : 0.0) + sum(b, B) / n;
-    } else {
-      const int q = f - 1 - B, i = q / B, j = q - i * B;
-      v = sum(i, j) - sum(i, B) * sum(j, B) / n;
+  const int tid = threadIdx.x, c = blockIdx.y;
+  // ranges that saw class c, ascending (one warp compacts)
+  if (tid < 32) {
+    int n = 0;
+    for (int g0 = 0; g0 < G; g0 += 32) {
+      const int g = g0 + tid;
+      const bool has = g < G && ((cmask[g] >> c) & 1u);
+      const unsigned bal = __ballot_sync(0xffffffffu, has);
+      if (has) act[n + __popc(bal & ((1u << tid) - 1u))] = g;
+      n += __popc(bal);
     }
+    if (tid == 0) nact_sh = n;
   }
-  if (lane == 0) moments[(size_t)(L.c0 + c) * len + f] = v;
+  __syncthreads();
+  const int nact = nact_sh;
+  int e = -1;
+  if (tid < kMergeEnt) {
+    const int t = blockIdx.x * kMergeEnt + tid;
+    if (t < E) e = t;
+  } else if (tid - kMergeEnt < R) {
+    e = ent_index(tid - kMergeEnt, B, R);
+  }
+  double sum = 0.0;
+  if (e >= 0) {
+    const double* p = part + (size_t)c * E + e;
+    const size_t stride = (size_t)C * E;
+    int a = 0;
+    for (; a + 4 <= nact; a += 4) {   // loads first, adds in range order
+      const double v0 = p[act[a] * stride], v1 = p[act[a + 1] * stride];
+      const double v2 = p[act[a + 2] * stride], v3 = p[act[a + 3] * stride];
+      sum += v0;
+      sum += v1;
+      sum += v2;
+      sum += v3;
+    }
+    for (; a < nact; ++a) sum += p[act[a] * stride];
+  }
+  if (tid >= kMergeEnt && tid - kMergeEnt < R) ones[tid - kMergeEnt] = sum;
+  __syncthreads();
+  if (tid >= kMergeEnt || e < 0) return;
+  // e -> (i, j), i <= j
+  int i = 0, rem = e;
+  while (rem >= R - i) { rem -= R - i; ++i; }
+  const int j = i + rem;
+  const double n = ones[B];
+  double* out = moments + (size_t)(L.c0 + c) * len;
+  if (j == B) {
+    if (i == B) {
+      out[0] = n > 0.0 ? n : 0.0;
+    } else {
+      out[1 + i] = n > 0.0 ? pivval[c * B + i] + sum / n : 0.0;
+    }
+  } else {
+    const double v = n > 0.0 ? sum - ones[i] * ones[j] / n : 0.0;
+    out[1 + B + i * B + j] = v;
+    out[1 + B + j * B + i] = v;
+  }
 }
 
 Layout make_layout(int64_t n, int b, int c) {
@@ -374,7 +464,8 @@ Layout make_layout(int64_t n, int b, int c) {
 
 size_t ws_bytes_for(int b, int c) {
   const int per = c < kMaxClasses ? c : kMaxClasses;
-  return sizeof(double) * (size_t)per * ent_count(b) * kMaxG + 256 + sizeof(int32_t) * 64;
+  return sizeof(double) * (size_t)per * ent_count(b) * kMaxG + 256 + sizeof(int32_t) * 64 +
+         sizeof(uint32_t) * kMaxG + sizeof(double) * kMaxClasses * kMaxBands;
 }
 
 template <typename Src>
@@ -388,6 +479,9 @@ int launch_moments(const Src& src, const int32_t* cls, int64_t n, int b, int cla
   if (int rc = ensure_smem(attr, moments_kernel<Src>, (size_t)full, "moments smem attribute")) return rc;
   int32_t* pivots = reinterpret_cast<int32_t*>(ws);
   double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + 256 + sizeof(int32_t) * 64);
+  const int per = classes < kMaxClasses ? classes : kMaxClasses;
+  uint32_t* cmask = reinterpret_cast<uint32_t*>(part + (size_t)per * ent_count(b) * kMaxG);
+  double* pivval = reinterpret_cast<double*>(cmask + kMaxG);
   for (int c0 = 0; c0 < classes; c0 += kMaxClasses) {
     Layout L = make_layout(n, b, classes - c0 < kMaxClasses ? classes - c0 : kMaxClasses);
     L.c0 = c0;
@@ -397,10 +491,10 @@ int launch_moments(const Src& src, const int32_t* cls, int64_t n, int b, int cla
       UT_CHECK_LAUNCH("pivot_kernel");
     }
     moments_kernel<Src><<<L.G, kThreads, smem_bytes(b, L.classes), st>>>(src, cls, piv, L, part,
-                                                                        first_bad);
+                                                                        cmask, pivval, first_bad);
     UT_CHECK_LAUNCH("moments_kernel");
-    const int64_t warps = (int64_t)L.classes * rec_len(b);
-    merge_kernel<Src><<<(int)((warps + 7) / 8), 256, 0, st>>>(src, part, piv, L, moments);
+    const dim3 mgrid((unsigned)((ent_count(b) + kMergeEnt - 1) / kMergeEnt), (unsigned)L.classes);
+    merge_kernel<<<mgrid, kMergeThreads, 0, st>>>(part, cmask, pivval, L, moments);
     UT_CHECK_LAUNCH("merge_kernel");
   }
   return UT_OK;

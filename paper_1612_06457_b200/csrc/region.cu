@@ -511,6 +511,9 @@ constexpr int kImP = 256;                 // pixels per tile
 #ifndef UT_IM_SLEEP  // suspend-time hint (ns) of the ring waits; 0 = spin on try_wait
 #define UT_IM_SLEEP 0
 #endif
+#ifndef UT_IM_EPI_SLEEP  // ns between polls of the epilogue warps' accumulator waits; 0 = spin
+#define UT_IM_EPI_SLEEP 0
+#endif
 #ifndef UT_IM_DSUM   // independent fp64 accumulators of the converters' sample sums
 #define UT_IM_DSUM 1
 #endif
@@ -573,7 +576,10 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
 
 // kind::i8 instruction descriptor: s32 accumulate, unsigned A and B, both K-major,
 // N = 144, M = 128.
-constexpr uint32_t kImIdesc = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(kImRows >> 3) << 17) |
+#ifndef UT_IM_PROBE_N    // dev probe (timing only): N of the MMA; B starts at row 144 - N
+#define UT_IM_PROBE_N kImRows
+#endif
+constexpr uint32_t kImIdesc = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(UT_IM_PROBE_N >> 3) << 17) |
                               ((uint32_t)(128 >> 4) << 24);
 
 __device__ __forceinline__ void tc_fence_after() {
@@ -744,7 +750,8 @@ region_imma_kernel(ImParams r) {
 #pragma unroll
         for (int kk = 0; kk < kImOpP / 32; ++kk) {
           const uint64_t d = umma_desc(base + (uint32_t)(kk * 2 * kImChunk));
-          tc_mma_i8(tmem + (uint32_t)(a * 256), d, d, (first && kk == 0) ? 0u : 1u);
+          const uint64_t db = umma_desc(base + (uint32_t)(kk * 2 * kImChunk) + (uint32_t)((kImRows - UT_IM_PROBE_N) * 16));
+          tc_mma_i8(tmem + (uint32_t)(a * 256), d, db, (first && kk == 0) ? 0u : 1u);
         }
         tc_commit(&op_empty[o]);
         if (last) tc_commit(&acc_full[a]);
@@ -770,7 +777,11 @@ region_imma_kernel(ImParams r) {
       for (int q = 0; q <= kMaxBands; ++q) rec[q] = 0;
     auto flush = [&](int w) {  // fold window w's TMEM accumulator into rec (int64)
       const int a = w & 1;
+#if UT_IM_EPI_SLEEP > 0
+      while (!mbar_test(&acc_full[a], (w >> 1) & 1)) __nanosleep(UT_IM_EPI_SLEEP);
+#else
       mbar_wait(&acc_full[a], (w >> 1) & 1);
+#endif
       tc_fence_after();
       const uint32_t t0 = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(a * 256);
 #pragma unroll
@@ -861,7 +872,11 @@ region_imma_kernel(ImParams r) {
           if ((o0[0] ^ o1[1] ^ o2[2] ^ o3[3]) == 0x12345678u) dst[0] = make_uint4(o0[1], o1[2], o2[3], o3[0]);
 #else
 #pragma unroll
+#ifdef UT_IM_PROBE_SKIPD0   // dev probe (timing only): three stored digits
+          for (int d = 1; d < 4; ++d) dst[32 * d] = make_uint4(o0[d], o1[d], o2[d], o3[d]);
+#else
           for (int d = 0; d < 4; ++d) dst[32 * d] = make_uint4(o0[d], o1[d], o2[d], o3[d]);
+#endif
 #endif
         }
       }
