@@ -280,15 +280,26 @@ int ut_encode_tiff(const void* img, int64_t rows, int64_t cols, int32_t channels
  * cv2.imread for TIFF bands.  src: the file's bytes in device memory; strip i
  * is in_len[i] bytes at in_off[i] and decodes to out_len[i] bytes at
  * dst + out_off[i] (all four arrays device).  compression 1 = raw strips,
- * 8 = one zlib stream per strip (Adler-32 checked).  status[i] (device) = 0,
- * or nonzero if strip i is malformed / too short / too long.
+ * 5 = TIFF LZW, 8 = one zlib stream per strip (Adler-32 checked).  status[i]
+ * (device) = 0, or nonzero if strip i is malformed / too short / too long.
+ * Tiles of a tiled TIFF and the IDAT stream of a PNG are streams too.
  * ut_unpredict undoes TIFF Predictor 2 (horizontal differencing per channel)
- * in place, after swapping the bytes of big-endian 16-bit samples if asked. */
+ * in place, after swapping the bytes of big-endian 16-bit samples if asked.
+ * ut_untile scatters decoded tiles (tile t = row-major (ty, tx), tile_rows x
+ * tile_row_bytes bytes each, contiguous) into the image rows.
+ * ut_png_unfilter reconstructs n PNGs' inflated scanlines in place and writes
+ * the images: table (device) holds, per image, work_off, out_off, rows, cols,
+ * channels (1 / 3), depth (8 / 16); 16-bit samples come out little endian;
+ * status[i] != 0 if image i has an invalid filter byte. */
 int ut_decode_strips(const uint8_t* src, const int64_t* in_off, const int64_t* in_len, int64_t nstrips,
                      int32_t compression, uint8_t* dst, const int64_t* out_off, const int64_t* out_len,
                      int32_t* status, void* stream);
 int ut_unpredict(void* img, int32_t depth, int64_t rows, int64_t cols, int32_t channels,
                  int32_t predictor, int32_t swap_bytes, void* stream);
+int ut_untile(const uint8_t* tiles, uint8_t* img, int64_t rows, int64_t row_bytes, int64_t tile_rows,
+              int64_t tile_row_bytes, int64_t tiles_across, int64_t ntiles, void* stream);
+int ut_png_unfilter(uint8_t* work, const int64_t* table, int64_t n, uint8_t* out, int32_t* status,
+                    void* stream);
 
 /* ------------------------------------------------- collectives (row shards)
  * SURVEY.md §8(b) ut_allreduce_f64 / §8(e): the sharded path's two exchange

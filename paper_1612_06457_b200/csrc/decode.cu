@@ -11,9 +11,22 @@
 //    zlib stream: RFC 1951 stored / fixed / dynamic blocks, canonical Huffman
 //    decoding by code length (count/symbol tables per stream), back-references
 //    from the stream's own output, Adler-32 verified;
+//  * lzw_kernel: LZW strips / tiles (Compression 5, MSB-first codes of 9..12
+//    bits with the TIFF "early change"), one thread per stream; a table entry is
+//    (position, length) of the string's first occurrence in the stream's own
+//    output, so the table costs 6 bytes per code and strings copy forward;
 //  * unpredict_kernel: TIFF Predictor 2 (horizontal differencing) undone per
 //    row and channel, after an optional byte swap of big-endian ('MM') 16-bit
-//    samples.
+//    samples;
+//  * untile_kernel: decoded tiles (Tile* tags) scattered into the image rows;
+//  * png_unfilter_kernel: the scanline filters of a PNG (None / Sub / Up /
+//    Average / Paeth; the IDAT zlib stream is inflated by inflate_kernel), one
+//    warp per image running a skewed wavefront over 32 rows at a time -- lane t
+//    reconstructs row y0 + t one pixel behind lane t - 1, the "up" pixel arrives
+//    by shuffle -- so the row-to-row and left-to-right dependencies of Average /
+//    Paeth cost (width + 32) steps per 32 rows instead of 32 x width;
+//    png_rows_kernel then drops the filter bytes and swaps 16-bit samples to
+//    little endian.
 // A stream whose data is malformed, too short or too long sets its status
 // word (and the caller raises DataError, as cv2.imread failing does).
 #include "common.cuh"
@@ -259,6 +272,220 @@ __global__ void __launch_bounds__(256) strips_copy_kernel(const uint8_t* __restr
   }
 }
 
+
+// ------------------------------------------------------------------ TIFF LZW
+// One LZW stream -> out[0, out_len).  pos / len: per-code string position and
+// length in `out` (codes >= 258).
+__device__ int lzw_one(const uint8_t* in, int64_t in_len, uint8_t* out, int64_t out_len,
+                       int32_t* pos, uint16_t* len) {
+  uint64_t buf = 0;   // MSB-first: the next code sits in the top bits
+  int cnt = 0;
+  int64_t ip = 0, o = 0;
+  int width = 9, next = 258, prev = -1;
+  int64_t prev_at = 0;
+  int prev_len = 0;
+  for (;;) {
+    while (cnt <= 56 && ip < in_len) {
+      buf |= (uint64_t)in[ip++] << (56 - cnt);
+      cnt += 8;
+    }
+    if (cnt < width) break;                    // data ended without EOI: accepted if complete
+    const int code = (int)(buf >> (64 - width));
+    buf <<= width;
+    cnt -= width;
+    if (code == 257) break;                    // EOI
+    if (code == 256) {                         // Clear
+      width = 9;
+      next = 258;
+      prev = -1;
+      continue;
+    }
+    int64_t at;
+    int n;
+    if (code < 256) {
+      if (o >= out_len) return kLong;
+      at = o;
+      n = 1;
+      out[o++] = (uint8_t)code;
+    } else {
+      if (prev < 0) return kBad;
+      int64_t from;
+      if (code < next) {
+        from = pos[code];
+        n = len[code];
+      } else if (code == next) {               // KwKwK: previous string + its first byte
+        from = prev_at;
+        n = prev_len + 1;
+      } else {
+        return kBad;
+      }
+      if (o + n > out_len) return kLong;
+      at = o;
+      for (int k = 0; k < n; ++k) out[o + k] = out[from + k];
+      o += n;
+    }
+    if (prev >= 0 && next < 4096) {            // new entry: previous string + first byte of this one
+      if (prev_len + 1 > 65535) return kBad;
+      pos[next] = (int32_t)prev_at;
+      len[next] = (uint16_t)(prev_len + 1);
+      ++next;
+    }
+    prev = code;
+    prev_at = at;
+    prev_len = n;
+    // early change: the width grows one code before the table fills the current width
+    if (next + 1 >= (1 << width) && width < 12) ++width;
+  }
+  return o == out_len ? 0 : kShort;
+}
+
+constexpr int kLzwThreads = 32;
+__global__ void __launch_bounds__(kLzwThreads) lzw_kernel(const uint8_t* __restrict__ src, const int64_t* in_off,
+                                                          const int64_t* in_len, int64_t n, uint8_t* dst,
+                                                          const int64_t* out_off, const int64_t* out_len,
+                                                          int32_t* status, int32_t* pos_ws, uint16_t* len_ws) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  status[i] = out_len[i] >= ((int64_t)1 << 31)
+                  ? kLong
+                  : lzw_one(src + in_off[i], in_len[i], dst + out_off[i], out_len[i], pos_ws + i * 4096,
+                            len_ws + i * 4096);
+}
+
+// ------------------------------------------------------------------ tiles
+// tile t = (ty, tx) holds tile_rows x tile_row_bytes bytes; the image gets the part inside it
+__global__ void __launch_bounds__(256) untile_kernel(const uint8_t* __restrict__ tiles, uint8_t* __restrict__ img,
+                                                     int64_t rows, int64_t row_bytes, int64_t tile_rows,
+                                                     int64_t tile_row_bytes, int64_t across) {
+  const int64_t t = blockIdx.x, ty = t / across, tx = t - ty * across;
+  const uint8_t* src = tiles + t * tile_rows * tile_row_bytes;
+  const int64_t y0 = ty * tile_rows, b0 = tx * tile_row_bytes;
+  const int64_t nr = rows - y0 < tile_rows ? rows - y0 : tile_rows;
+  const int64_t nb = row_bytes - b0 < tile_row_bytes ? row_bytes - b0 : tile_row_bytes;
+  for (int64_t e = threadIdx.x; e < nr * nb; e += blockDim.x) {
+    const int64_t r = e / nb, c = e - r * nb;
+    img[(y0 + r) * row_bytes + b0 + c] = src[r * tile_row_bytes + c];
+  }
+}
+
+// ------------------------------------------------------------------ PNG filters
+constexpr int kPngCx = 32;        // pixel columns per staged chunk (>= 32: the wavefront spans two chunks)
+constexpr int kPngMaxBpp = 8;
+
+__device__ __forceinline__ uint32_t paeth(uint32_t a, uint32_t b, uint32_t c) {
+  const int pa = abs((int)b - (int)c), pb = abs((int)a - (int)c), pc = abs((int)a + (int)b - 2 * (int)c);
+  return (pa <= pb && pa <= pc) ? a : (pb <= pc ? b : c);
+}
+
+// table row i: work_off, out_off, rows, cols, channels, depth.  work holds the
+// inflated scanlines ([filter byte][row bytes] per row); they are reconstructed
+// in place.  One warp per image.
+__global__ void __launch_bounds__(32) png_unfilter_kernel(uint8_t* __restrict__ work,
+                                                          const int64_t* __restrict__ table,
+                                                          int32_t* __restrict__ status) {
+  __shared__ uint8_t sin[2][33][kPngCx * kPngMaxBpp];   // row 32 = the row above the group
+  __shared__ uint8_t sout[2][32][kPngCx * kPngMaxBpp];
+  const int64_t* tb = table + (int64_t)blockIdx.x * 6;
+  const int64_t rows = tb[2], cols = tb[3];
+  const int bpp = (int)(tb[4] * tb[5] / 8);
+  const int64_t rb = cols * bpp, stride = rb + 1;
+  uint8_t* base = work + tb[0];
+  const int lane = threadIdx.x;
+  const int64_t nchunks = (cols + kPngCx - 1) / kPngCx;
+  int bad = 0;
+  for (int64_t y0 = 0; y0 < rows; y0 += 32) {
+    const int64_t y = y0 + lane;
+    const bool live = y < rows;
+    const int ft = live ? base[y * stride] : 0;
+    if (ft > 4) bad = 1;
+    uint32_t a[kPngMaxBpp], b[kPngMaxBpp], c[kPngMaxBpp];
+#pragma unroll
+    for (int j = 0; j < kPngMaxBpp; ++j) a[j] = b[j] = c[j] = 0;
+    auto load_chunk = [&](int64_t k) {   // filtered bytes of chunk k of the 32 rows + the row above
+      const int buf = (int)(k & 1);
+      const int64_t c0 = k * kPngCx * bpp;
+      const int nb = (int)((rb - c0) < (int64_t)kPngCx * bpp ? (rb - c0) : (int64_t)kPngCx * bpp);
+      for (int r = 0; r < 33; ++r) {
+        const int64_t yy = r < 32 ? y0 + r : y0 - 1;
+        if (yy < 0 || yy >= rows) {
+          if (r == 32) for (int e = lane; e < nb; e += 32) sin[buf][r][e] = 0;
+          continue;
+        }
+        const uint8_t* src = base + yy * stride + 1 + c0;
+        for (int e = lane; e < nb; e += 32) sin[buf][r][e] = src[e];
+      }
+    };
+    auto flush_chunk = [&](int64_t k) {  // reconstructed bytes of chunk k back in place
+      const int buf = (int)(k & 1);
+      const int64_t c0 = k * kPngCx * bpp;
+      const int nb = (int)((rb - c0) < (int64_t)kPngCx * bpp ? (rb - c0) : (int64_t)kPngCx * bpp);
+      for (int r = 0; r < 32 && y0 + r < rows; ++r) {
+        uint8_t* dst = base + (y0 + r) * stride + 1 + c0;
+        for (int e = lane; e < nb; e += 32) dst[e] = sout[buf][r][e];
+      }
+    };
+    const int64_t steps = cols + 31;
+    for (int64_t s = 0; s < steps; ++s) {
+      if (s % kPngCx == 0) {
+        const int64_t k = s / kPngCx;
+        __syncwarp();
+        if (k >= 2) flush_chunk(k - 2);
+        if (k < nchunks) load_chunk(k);
+        __syncwarp();
+      }
+      // the pixel lane - 1 produced last step is this lane's "up" pixel
+      uint32_t up[kPngMaxBpp];
+#pragma unroll
+      for (int j = 0; j < kPngMaxBpp; ++j) up[j] = __shfl_up_sync(0xffffffffu, a[j], 1);
+      const int64_t x = s - lane;
+      if (live && x >= 0 && x < cols) {
+        const int buf = (int)((x / kPngCx) & 1);
+        const int xc = (int)(x % kPngCx) * bpp;
+#pragma unroll
+        for (int j = 0; j < kPngMaxBpp; ++j) {
+          if (j < bpp) {
+            c[j] = x == 0 ? 0u : b[j];
+            b[j] = lane == 0 ? (uint32_t)sin[buf][32][xc + j] : up[j];
+            const uint32_t left = x == 0 ? 0u : a[j];
+            uint32_t pred = 0;
+            if (ft == 1) pred = left;
+            else if (ft == 2) pred = b[j];
+            else if (ft == 3) pred = (left + b[j]) >> 1;
+            else if (ft == 4) pred = paeth(left, b[j], c[j]);
+            a[j] = ((uint32_t)sin[buf][lane][xc + j] + pred) & 0xffu;
+            sout[buf][lane][xc + j] = (uint8_t)a[j];
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (nchunks >= 2) flush_chunk(nchunks - 2);
+    flush_chunk(nchunks - 1);
+    __syncwarp();
+    __threadfence_block();
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) status[blockIdx.x] = bad ? kBad : 0;
+}
+
+// reconstructed scanlines -> image rows (filter byte dropped, 16-bit samples to little endian)
+__global__ void __launch_bounds__(256) png_rows_kernel(const uint8_t* __restrict__ work,
+                                                       const int64_t* __restrict__ table,
+                                                       uint8_t* __restrict__ out) {
+  const int64_t* tb = table + (int64_t)blockIdx.y * 6;
+  const int64_t rows = tb[2], cols = tb[3];
+  const int bpp = (int)(tb[4] * tb[5] / 8);
+  const bool swap = tb[5] == 16;
+  const int64_t rb = cols * bpp, stride = rb + 1;
+  const uint8_t* base = work + tb[0];
+  uint8_t* dst = out + tb[1];
+  for (int64_t y = blockIdx.x; y < rows; y += gridDim.x) {
+    const uint8_t* src = base + y * stride + 1;
+    uint8_t* d = dst + y * rb;
+    for (int64_t e = threadIdx.x; e < rb; e += blockDim.x) d[e] = src[swap ? (e ^ 1) : e];
+  }
+}
+
 template <typename T>
 __global__ void unpredict_kernel(T* img, int64_t rows, int64_t spr, int ch, int predictor, int swap) {
   const int64_t y = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -284,14 +511,27 @@ int ut_decode_strips(const uint8_t* src, const int64_t* in_off, const int64_t* i
                      int32_t compression, uint8_t* dst, const int64_t* out_off, const int64_t* out_len,
                      int32_t* status, void* stream) {
   UT_REQUIRE(nstrips >= 0, "negative strip count");
-  UT_REQUIRE(compression == 1 || compression == 8,
-             "strip compression must be 1 (none) or 8 (zlib deflate), got %d", compression);
+  UT_REQUIRE(compression == 1 || compression == 8 || compression == 5,
+             "strip compression must be 1 (none), 5 (LZW) or 8 (zlib deflate), got %d", compression);
   if (nstrips == 0) return UT_OK;
   UT_REQUIRE(src && in_off && in_len && dst && out_off && out_len && status, "ut_decode_strips: null pointer");
   cudaStream_t st = as_stream(stream);
   if (compression == 1) {
     strips_copy_kernel<<<(unsigned)nstrips, 256, 0, st>>>(src, in_off, in_len, dst, out_off, out_len, status);
     UT_CHECK_LAUNCH("strips_copy_kernel");
+  } else if (compression == 5) {
+    // string tables: 6 bytes per code and stream, stream-ordered scratch
+    void* tab = nullptr;
+    const size_t per = 4096 * (sizeof(int32_t) + sizeof(uint16_t));
+    cudaError_t e = cudaMallocAsync(&tab, per * (size_t)nstrips, st);
+    if (e != cudaSuccess) return cuda_status(e, "ut_decode_strips: LZW tables");
+    int32_t* pos = static_cast<int32_t*>(tab);
+    uint16_t* len = reinterpret_cast<uint16_t*>(pos + (size_t)nstrips * 4096);
+    lzw_kernel<<<(unsigned)((nstrips + kLzwThreads - 1) / kLzwThreads), kLzwThreads, 0, st>>>(
+        src, in_off, in_len, nstrips, dst, out_off, out_len, status, pos, len);
+    const cudaError_t le = cudaGetLastError();
+    cudaFreeAsync(tab, st);
+    if (le != cudaSuccess) return cuda_status(le, "lzw_kernel");
   } else {
     inflate_kernel<<<(unsigned)((nstrips + kInfThreads - 1) / kInfThreads), kInfThreads, 0, st>>>(
         src, in_off, in_len, nstrips, dst, out_off, out_len, status);
@@ -315,6 +555,32 @@ int ut_unpredict(void* img, int32_t depth, int64_t rows, int64_t cols, int32_t c
     unpredict_kernel<uint16_t><<<grid, 128, 0, st>>>(static_cast<uint16_t*>(img), rows, cols * channels,
                                                      channels, predictor, swap_bytes);
   UT_CHECK_LAUNCH("unpredict_kernel");
+  return UT_OK;
+}
+
+int ut_untile(const uint8_t* tiles, uint8_t* img, int64_t rows, int64_t row_bytes, int64_t tile_rows,
+              int64_t tile_row_bytes, int64_t tiles_across, int64_t ntiles, void* stream) {
+  UT_REQUIRE(rows > 0 && row_bytes > 0 && tile_rows > 0 && tile_row_bytes > 0 && tiles_across > 0,
+             "ut_untile: bad geometry");
+  UT_REQUIRE(ntiles >= 0 && ntiles < ((int64_t)1 << 31), "ut_untile: bad tile count");
+  if (ntiles == 0) return UT_OK;
+  UT_REQUIRE(tiles && img, "ut_untile: null pointer");
+  untile_kernel<<<(unsigned)ntiles, 256, 0, as_stream(stream)>>>(tiles, img, rows, row_bytes, tile_rows,
+                                                                tile_row_bytes, tiles_across);
+  UT_CHECK_LAUNCH("untile_kernel");
+  return UT_OK;
+}
+
+int ut_png_unfilter(uint8_t* work, const int64_t* table, int64_t n, uint8_t* out, int32_t* status,
+                    void* stream) {
+  UT_REQUIRE(n >= 0 && n < 65536, "ut_png_unfilter: bad image count");
+  if (n == 0) return UT_OK;
+  UT_REQUIRE(work && table && out && status, "ut_png_unfilter: null pointer");
+  cudaStream_t st = as_stream(stream);
+  png_unfilter_kernel<<<(unsigned)n, 32, 0, st>>>(work, table, status);
+  UT_CHECK_LAUNCH("png_unfilter_kernel");
+  png_rows_kernel<<<dim3(64, (unsigned)n), 256, 0, st>>>(work, table, out);
+  UT_CHECK_LAUNCH("png_rows_kernel");
   return UT_OK;
 }
 

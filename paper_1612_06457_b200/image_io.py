@@ -190,10 +190,15 @@ def save_image(img, path: str | Path, compression: str = "none") -> None:
 # ------------------------------------------------------------------ decode
 
 _TIFF_TYPES = {1: ("B", 1), 3: ("H", 2), 4: ("I", 4), 16: ("Q", 8)}
+_TIFF_CODES = {1: 1, 5: 5, 8: 8, 32946: 8}      # Compression tag -> decoder (raw, LZW, zlib)
 
 
 class _Unsupported(Exception):
-    """A file layout the device decoder does not handle (the caller uses cv2)."""
+    """A file layout the device decoders do not handle (the caller uses cv2)."""
+
+
+def _align(n: int, a: int = 256) -> int:
+    return -(-int(n) // a) * a
 
 
 def _tiff_layout(data: bytes) -> dict:
@@ -221,10 +226,16 @@ def _tiff_layout(data: bytes) -> dict:
         "compression": get(259, 1)[0], "photometric": get(262, 1)[0], "spp": get(277, 1)[0],
         "rps": get(278, 2 ** 32 - 1)[0], "planar": get(284, 1)[0], "predictor": get(317, 1)[0],
         "format": get(339, 1)[0], "offsets": tags.get(273), "counts": tags.get(279),
+        "tile_w": get(322)[0], "tile_h": get(323)[0],
+        "tile_offsets": tags.get(324), "tile_counts": tags.get(325),
     }
-    if 322 in tags or lay["offsets"] is None or lay["counts"] is None:
-        raise _Unsupported("tiled or strip-less TIFF")
-    if lay["compression"] not in (1, 8, 32946) or lay["predictor"] not in (1, 2):
+    lay["tiled"] = lay["tile_w"] is not None
+    if lay["tiled"]:
+        if lay["tile_h"] is None or lay["tile_offsets"] is None or lay["tile_counts"] is None:
+            raise _Unsupported("incomplete tile tags")
+    elif lay["offsets"] is None or lay["counts"] is None:
+        raise _Unsupported("strip-less TIFF")
+    if lay["compression"] not in _TIFF_CODES or lay["predictor"] not in (1, 2):
         raise _Unsupported(f"compression {lay['compression']} / predictor {lay['predictor']}")
     if len(set(lay["bps"])) != 1 or lay["bps"][0] not in (8, 16) or lay["format"] != 1:
         raise _Unsupported("sample type")
@@ -236,48 +247,118 @@ def _tiff_layout(data: bytes) -> dict:
 
 
 def _tiff_plan(data: bytes) -> dict:
-    """Geometry and strip tables of a device-decodable TIFF (host)."""
+    """Geometry and stream tables of a device-decodable TIFF (host).  Streams
+    are the strips, or the tiles (decoded into a scratch area behind the image
+    and scattered into its rows afterwards)."""
     lay = _tiff_layout(data)
     h, w, ch = int(lay["height"]), int(lay["width"]), int(lay["spp"])
     depth = int(lay["bps"][0])
-    rb = w * ch * depth // 8
-    rps = min(int(lay["rps"]), h)
-    nstrips = -(-h // rps)
-    offs = np.asarray(lay["offsets"], dtype=np.int64)
-    counts = np.asarray(lay["counts"], dtype=np.int64)
-    if len(offs) != nstrips or len(counts) != nstrips:
-        raise DataError(f"TIFF lists {len(offs)} strips, expected {nstrips}")
+    px = ch * depth // 8
+    rb = w * px
+    plan = {"kind": "tiff", "payload": data, "h": h, "w": w, "ch": ch, "depth": depth,
+            "bytes": h * rb, "code": _TIFF_CODES[lay["compression"]],
+            "predictor": int(lay["predictor"]), "swap": int(lay["bo"] == ">" and depth == 16),
+            "tiled": bool(lay["tiled"])}
+    if lay["tiled"]:
+        tw, th = int(lay["tile_w"]), int(lay["tile_h"])
+        if tw <= 0 or th <= 0:
+            raise DataError("TIFF tile size must be positive")
+        across, down = -(-w // tw), -(-h // th)
+        n = across * down
+        offs = np.asarray(lay["tile_offsets"], dtype=np.int64)
+        counts = np.asarray(lay["tile_counts"], dtype=np.int64)
+        if len(offs) != n or len(counts) != n:
+            raise DataError(f"TIFF lists {len(offs)} tiles, expected {n}")
+        tile_bytes = th * tw * px
+        scratch0 = _align(h * rb)
+        plan.update(tile_w=tw, tile_h=th, across=across, ntiles=n, scratch=scratch0,
+                    out_off=scratch0 + np.arange(n, dtype=np.int64) * tile_bytes,
+                    out_len=np.full(n, tile_bytes, dtype=np.int64),
+                    region=scratch0 + _align(n * tile_bytes))
+    else:
+        rps = min(int(lay["rps"]), h)
+        n = -(-h // rps)
+        offs = np.asarray(lay["offsets"], dtype=np.int64)
+        counts = np.asarray(lay["counts"], dtype=np.int64)
+        if len(offs) != n or len(counts) != n:
+            raise DataError(f"TIFF lists {len(offs)} strips, expected {n}")
+        out_len = np.full(n, rps * rb, dtype=np.int64)
+        out_len[-1] = (h - (n - 1) * rps) * rb
+        plan.update(out_off=np.arange(n, dtype=np.int64) * rps * rb, out_len=out_len,
+                    region=_align(h * rb))
     if int((offs + counts).max()) > len(data):
         raise DataError("TIFF strip runs past the end of the file")
-    out_len = np.full(nstrips, rps * rb, dtype=np.int64)
-    out_len[-1] = (h - (nstrips - 1) * rps) * rb
-    return {"h": h, "w": w, "ch": ch, "depth": depth, "bytes": h * rb, "offs": offs,
-            "counts": counts, "out_off": np.arange(nstrips, dtype=np.int64) * rps * rb,
-            "out_len": out_len, "code": 1 if lay["compression"] == 1 else 8,
-            "predictor": int(lay["predictor"]), "swap": int(lay["bo"] == ">" and depth == 16)}
+    plan.update(offs=offs, counts=counts)
+    return plan
 
 
-def decode_tiff_batch(datas: list, device=None) -> list:
-    """Device planes of several stripped TIFFs (raw or deflate, Predictor 1 / 2,
-    either byte order) with one staging copy and one decode launch per
-    compression kind, so every strip of every file decodes in parallel.
-    Raises _Unsupported if any file has another layout."""
-    plans = [_tiff_plan(d) for d in datas]
+def _png_plan(data: bytes) -> dict:
+    """Geometry of a device-decodable PNG (host: chunk walk only).  Grayscale or
+    RGB, 8 or 16 bits, not interlaced, no transparency chunk; the payload staged
+    to the device is the IDAT chunks' zlib stream."""
+    if data[:8] != _PNG_SIGNATURE:
+        raise _Unsupported("not a PNG")
+    at, ihdr, idat, seen_end = 8, None, [], False
+    while at + 12 <= len(data):
+        (n,) = struct.unpack(">I", data[at:at + 4])
+        kind = data[at + 4:at + 8]
+        body_at = at + 8
+        if body_at + n + 4 > len(data):
+            raise DataError("PNG chunk runs past the end of the file")
+        if kind == b"IHDR":
+            ihdr = struct.unpack(">IIBBBBB", data[body_at:body_at + 13])
+        elif kind == b"IDAT":
+            idat.append(data[body_at:body_at + n])
+        elif kind in (b"tRNS", b"PLTE"):
+            raise _Unsupported("palette / transparency")
+        elif kind == b"IEND":
+            seen_end = True
+            break
+        at = body_at + n + 4
+    if ihdr is None or not idat or not seen_end:
+        raise DataError("PNG has no IHDR / IDAT / IEND chunk")
+    w, h, depth, color, comp, filt, interlace = ihdr
+    if color not in (0, 2) or depth not in (8, 16) or interlace != 0 or comp != 0 or filt != 0:
+        raise _Unsupported(f"PNG colour type {color}, depth {depth}, interlace {interlace}")
+    if w <= 0 or h <= 0:
+        raise DataError("PNG has an empty image")
+    ch = 3 if color == 2 else 1
+    rb = w * ch * depth // 8
+    work0 = _align(h * rb)
+    return {"kind": "png", "payload": b"".join(idat), "h": h, "w": w, "ch": ch, "depth": depth,
+            "bytes": h * rb, "code": 8, "work": work0, "region": work0 + _align(h * (rb + 1)),
+            "offs": np.zeros(1, dtype=np.int64), "counts": np.asarray([sum(map(len, idat))], dtype=np.int64),
+            "out_off": np.asarray([work0], dtype=np.int64),
+            "out_len": np.asarray([h * (rb + 1)], dtype=np.int64)}
+
+
+def _plan(data: bytes) -> dict:
+    if data[:8] == _PNG_SIGNATURE:
+        return _png_plan(data)
+    return _tiff_plan(data)
+
+
+def decode_batch(datas: list, device=None) -> list:
+    """Device planes of several image files -- TIFFs (strips or tiles; raw, LZW
+    or deflate; Predictor 1 / 2; either byte order) and PNGs (grayscale / RGB,
+    8 / 16 bit) -- with one staging copy and one decode launch per compression
+    kind, so every stream of every file decodes in parallel (a PNG is one
+    stream).  Raises _Unsupported if any file has another layout."""
+    plans = [_plan(d) for d in datas]
     device = device or dev.require_cuda()
-    file_base = np.cumsum([0] + [len(d) for d in datas])
-    # each image starts on a 256-byte boundary (16-bit views need no copy)
-    out_base = np.cumsum([0] + [-(-pl["bytes"] // 256) * 256 for pl in plans])
+    file_base = np.cumsum([0] + [_align(len(pl["payload"]), 16) for pl in plans])
+    out_base = np.cumsum([0] + [pl["region"] for pl in plans])
     with torch.cuda.device(device):
-        host = torch.empty(int(file_base[-1]), dtype=torch.uint8, pin_memory=True)
+        host = torch.empty(int(file_base[-1]) + 16, dtype=torch.uint8, pin_memory=True)
         hv = host.numpy()
-        for d, b0 in zip(datas, file_base):
-            hv[b0:b0 + len(d)] = np.frombuffer(d, dtype=np.uint8)
+        for pl, b0 in zip(plans, file_base):
+            hv[b0:b0 + len(pl["payload"])] = np.frombuffer(pl["payload"], dtype=np.uint8)
         src = host.to(device, non_blocking=True)
         out = torch.empty(int(out_base[-1]) + 16, dtype=torch.uint8, device=device)
         L = _lib.lib()
         s = dev.stream_handle()
         statuses = []
-        for code in (1, 8):
+        for code in (1, 5, 8):
             sel = [i for i, pl in enumerate(plans) if pl["code"] == code]
             if not sel:
                 continue
@@ -293,30 +374,67 @@ def decode_tiff_batch(datas: list, device=None) -> list:
                                           tables[2].data_ptr(), tables[3].data_ptr(),
                                           status.data_ptr(), s), "ut_decode_strips")
             statuses.append(status)
+        pngs = [i for i, pl in enumerate(plans) if pl["kind"] == "png"]
+        if pngs:
+            table = torch.from_numpy(np.asarray(
+                [[out_base[i] + plans[i]["work"], out_base[i], plans[i]["h"], plans[i]["w"],
+                  plans[i]["ch"], plans[i]["depth"]] for i in pngs], dtype=np.int64)).to(device)
+            status = torch.empty(len(pngs), dtype=torch.int32, device=device)
+            _lib.check(L.ut_png_unfilter(out.data_ptr(), table.data_ptr(), len(pngs),
+                                         out.data_ptr(), status.data_ptr(), s), "ut_png_unfilter")
+            statuses.append(status)
         images = []
         for pl, o0 in zip(plans, out_base):
+            o0 = int(o0)
             dtype = torch.uint8 if pl["depth"] == 8 else torch.uint16
-            flat = out[int(o0):int(o0) + pl["bytes"]]
-            img = flat.view(dtype)
-            _lib.check(L.ut_unpredict(img.data_ptr(), pl["depth"], pl["h"], pl["w"], pl["ch"],
-                                      pl["predictor"], pl["swap"], s), "ut_unpredict")
+            img = out[o0:o0 + pl["bytes"]].view(dtype)
+            if pl["kind"] == "tiff" and pl["tiled"]:
+                # byte order and Predictor 2 are per tile row: undo them on the tiles
+                t0 = o0 + pl["scratch"]
+                tiles = out[t0:t0 + pl["ntiles"] * pl["tile_h"] * pl["tile_w"] * pl["ch"] * pl["depth"] // 8]
+                _lib.check(L.ut_unpredict(tiles.data_ptr(), pl["depth"], pl["ntiles"] * pl["tile_h"],
+                                          pl["tile_w"], pl["ch"], pl["predictor"], pl["swap"], s),
+                           "ut_unpredict")
+                px = pl["ch"] * pl["depth"] // 8
+                _lib.check(L.ut_untile(tiles.data_ptr(), img.data_ptr(), pl["h"], pl["w"] * px,
+                                       pl["tile_h"], pl["tile_w"] * px, pl["across"], pl["ntiles"], s),
+                           "ut_untile")
+            elif pl["kind"] == "tiff":
+                _lib.check(L.ut_unpredict(img.data_ptr(), pl["depth"], pl["h"], pl["w"], pl["ch"],
+                                          pl["predictor"], pl["swap"], s), "ut_unpredict")
             images.append(img.view(pl["h"], pl["w"], pl["ch"]) if pl["ch"] == 3
                           else img.view(pl["h"], pl["w"]))
         bad = sum(int((st != 0).sum().item()) for st in statuses)
     if bad:
-        raise DataError(f"TIFF data has {bad} undecodable strip(s)")
+        raise DataError(f"image data has {bad} undecodable stream(s)")
     return images
 
 
+def decode_tiff_batch(datas: list, device=None) -> list:
+    """Device planes of several TIFFs (see decode_batch)."""
+    for d in datas:
+        if d[:8] == _PNG_SIGNATURE:
+            raise _Unsupported("not a TIFF")
+    return decode_batch(datas, device)
+
+
 def decode_tiff(data: bytes, device=None) -> torch.Tensor:
-    """Device (H, W[, 3]) uint8 / uint16 planes of one stripped TIFF."""
+    """Device (H, W[, 3]) uint8 / uint16 planes of one TIFF."""
     return decode_tiff_batch([data], device)[0]
 
 
+def decode_png(data: bytes, device=None) -> torch.Tensor:
+    """Device (H, W[, 3]) uint8 / uint16 planes of one PNG."""
+    if data[:8] != _PNG_SIGNATURE:
+        raise _Unsupported("not a PNG")
+    return decode_batch([data], device)[0]
+
+
 def read_image_device(path: str | Path, device=None):
-    """(device tensor, decoded-on-device flag) for an image file: stripped
-    TIFFs decode on the B200; other files (PNG, LZW / tiled TIFF, ...) go
-    through cv2.imread on the host exactly as the reference reads them, then
+    """(device tensor, decoded-on-device flag) for an image file: TIFFs (strips
+    or tiles; raw / LZW / deflate) and PNGs (grayscale / RGB, 8 / 16 bit) decode
+    on the B200; other layouts (palette, interlaced, alpha, JPEG-in-TIFF, ...)
+    go through cv2.imread on the host exactly as the reference reads them, then
     to the device.  DataError if the file cannot be read."""
     path = Path(path)
     try:
@@ -324,7 +442,7 @@ def read_image_device(path: str | Path, device=None):
     except OSError:
         raise DataError(f"cannot read image {path}") from None
     try:
-        return decode_tiff(data, device), True
+        return decode_batch([data], device)[0], True
     except _Unsupported:
         pass
     import cv2  # the reference's decoder, for layouts the device path does not parse

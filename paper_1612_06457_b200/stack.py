@@ -279,9 +279,9 @@ def _parse_manifest_line(line: str, lineno: int, base: Path):
 
 
 def load_device_stack(manifest) -> DeviceStack:
-    """The bands named by a manifest, decoded into one HBM cube (stripped TIFF
+    """The bands named by a manifest, decoded into one HBM cube (TIFF and PNG
     bands decode on the device; see image_io.read_image_device)."""
-    from .image_io import _Unsupported, decode_tiff_batch, read_image_device
+    from .image_io import _Unsupported, decode_batch, read_image_device
 
     manifest = Path(manifest)
     if not manifest.is_file():
@@ -297,11 +297,12 @@ def load_device_stack(manifest) -> DeviceStack:
     for band_id, (path, _w, _i, _f) in enumerate(entries):
         if not path.is_file():
             raise DataError(f"band {band_id}: image file not found: {path}")
-    # all bands in one batched device decode when every file is a stripped TIFF
+    # all bands in one batched device decode when every file is a TIFF / PNG the
+    # device decoders parse
     imgs = None
     try:
         datas = [path.read_bytes() for path, *_ in entries]
-        imgs = decode_tiff_batch(datas)
+        imgs = decode_batch(datas)
     except (_Unsupported, DataError, OSError):
         imgs = None
     metas, planes = [], []

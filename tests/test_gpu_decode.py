@@ -1,10 +1,12 @@
 """load_stack / load_image on the device (stack.py:119-177, rendering.py:334-343;
-SURVEY §8(f) row 3): stripped TIFF bands -- as the reference's save_image
-writes them through cv2 (raw or deflate), as the device encoder writes them, and
-big-endian -- decode on the B200 to exactly what cv2.imread returns; the
-reference's load_stack cases (test_stack.py:53-113) hold."""
+SURVEY §8(f) row 3): TIFF bands -- as the reference's save_image writes them
+through cv2 (raw or deflate), as the device encoder writes them, big-endian, LZW
+(cv2's default TIFF compression) and tiled -- and PNGs (every scanline filter)
+decode on the B200 to exactly what cv2.imread returns; the reference's
+load_stack cases (test_stack.py:53-113) hold."""
 
 import struct
+import zlib
 
 import numpy as np
 import pytest
@@ -114,14 +116,216 @@ def test_corrupt_strip_raises(tmp_path):
         image_io.decode_tiff(bytes(data))
 
 
-def test_png_and_unsupported_layouts_use_the_reference_decoder(tmp_path):
-    img = image((40, 50), np.uint8, 5)
+def no_host_codecs(monkeypatch):
+    def boom(*args, **kwargs):
+        raise AssertionError("host codec called")
+
+    for name in ("imread", "imdecode", "imreadmulti"):
+        monkeypatch.setattr(cv2, name, boom)
+
+
+@pytest.mark.parametrize("shape,dtype", [((1, 1), np.uint8), ((20, 30), np.uint8),
+                                         ((513, 1031), np.uint8), ((300, 777), np.uint16),
+                                         ((64, 48, 3), np.uint8), ((65, 33, 3), np.uint16),
+                                         ((1200, 2000), np.uint16)])
+def test_cv2_written_png_decodes_on_device(tmp_path, shape, dtype):
+    img = image(shape, dtype, 11)
+    path = tmp_path / "a.png"
+    cv2_write(path, img)
+    want = cv2_read(path)
+    assert np.array_equal(want, img)
+    t = image_io.decode_png(path.read_bytes())           # the device path, no fallback
+    assert t.is_cuda and t.dtype == (torch.uint8 if dtype == np.uint8 else torch.uint16)
+    assert np.array_equal(t.cpu().numpy(), want)
+
+
+def _png_filter_rows(img, kinds):
+    """Scanlines of img (H, W[, 3]) filtered with the given per-row filter types
+    (PNG specification, section 9), 16-bit samples big endian."""
+    h = img.shape[0]
+    raw = img.astype(">u2" if img.dtype == np.uint16 else np.uint8).reshape(h, -1).view(np.uint8)
+    bpp = raw.shape[1] // img.shape[1]
+    out = bytearray()
+    prev = np.zeros(raw.shape[1], dtype=np.int32)
+    for y in range(h):
+        cur = raw[y].astype(np.int32)
+        left = np.concatenate([np.zeros(bpp, np.int32), cur[:-bpp]])
+        ul = np.concatenate([np.zeros(bpp, np.int32), prev[:-bpp]])
+        kind = kinds[y % len(kinds)]
+        if kind == 0:
+            pred = np.zeros_like(cur)
+        elif kind == 1:
+            pred = left
+        elif kind == 2:
+            pred = prev
+        elif kind == 3:
+            pred = (left + prev) >> 1
+        else:
+            p = left + prev - ul
+            pa, pb, pc = np.abs(p - left), np.abs(p - prev), np.abs(p - ul)
+            pred = np.where((pa <= pb) & (pa <= pc), left, np.where(pb <= pc, prev, ul))
+        out.append(kind)
+        out += ((cur - pred) & 0xFF).astype(np.uint8).tobytes()
+        prev = cur
+    return bytes(out)
+
+
+def _png_file(img, kinds, idat_split=1 << 30):
+    h, w = img.shape[:2]
+    color = 2 if img.ndim == 3 else 0
+    depth = 16 if img.dtype == np.uint16 else 8
+    chunk = lambda k, d: struct.pack(">I", len(d)) + k + d + struct.pack(">I", zlib.crc32(k + d))  # noqa: E731
+    z = zlib.compress(_png_filter_rows(img, kinds), 6)
+    idat = b"".join(chunk(b"IDAT", z[i:i + idat_split]) for i in range(0, len(z), idat_split))
+    return (b"\x89PNG\r\n\x1a\n" + chunk(b"IHDR", struct.pack(">IIBBBBB", w, h, depth, color, 0, 0, 0))
+            + chunk(b"tEXt", b"Comment\0hand-filtered") + idat + chunk(b"IEND", b""))
+
+
+@pytest.mark.parametrize("kinds", [[0], [1], [2], [3], [4], [4, 3, 2, 1, 0], [3, 4]])
+@pytest.mark.parametrize("shape,dtype", [((70, 45), np.uint8), ((37, 101), np.uint16),
+                                         ((40, 67, 3), np.uint8), ((33, 35, 3), np.uint16)])
+def test_every_png_filter(tmp_path, kinds, shape, dtype):
+    """Hand-filtered PNGs (each scanline filter alone and mixed, rows crossing
+    the 32-row wavefront groups, IDAT split over several chunks)."""
+    img = image(shape, dtype, 12)
+    data = _png_file(img, kinds, idat_split=997)
+    got = image_io.decode_png(data).cpu().numpy()
+    assert np.array_equal(got, img)
+    ref = cv2.imdecode(np.frombuffer(data, np.uint8), cv2.IMREAD_UNCHANGED)
+    assert np.array_equal(ref[:, :, ::-1] if ref.ndim == 3 else ref, img)
+
+
+def test_device_written_png_round_trip(tmp_path):
+    for shape, dtype in (((300, 200), np.uint16), ((90, 120, 3), np.uint8)):
+        img = image(shape, dtype, 13)
+        got = image_io.decode_png(image_io.encode_png(torch.from_numpy(img).cuda()))
+        assert np.array_equal(got.cpu().numpy(), img)
+
+
+def test_corrupt_png_raises():
+    img = image((120, 90), np.uint8, 14)
+    data = bytearray(_png_file(img, [4]))
+    at = data.index(b"IDAT") + 4
+    data[at + 20:at + 50] = bytes(30)
+    with pytest.raises(ut.DataError):
+        image_io.decode_png(bytes(data))
+    good = _png_file(img, [0])                     # the same image with a filter byte of 7
+    rows = bytearray(_png_filter_rows(img, [0]))
+    rows[0] = 7
+    chunk = lambda k, d: struct.pack(">I", len(d)) + k + d + struct.pack(">I", zlib.crc32(k + d))  # noqa: E731
+    head = good[:good.index(b"IDAT") - 4]
+    with pytest.raises(ut.DataError):
+        image_io.decode_png(head + chunk(b"IDAT", zlib.compress(bytes(rows))) + chunk(b"IEND", b""))
+
+
+@pytest.mark.parametrize("shape,dtype", [((1, 1), np.uint8), ((20, 30), np.uint8),
+                                         ((513, 1031), np.uint8), ((300, 777), np.uint16),
+                                         ((64, 48, 3), np.uint8), ((1200, 2000), np.uint16)])
+def test_cv2_written_lzw_tiff_decodes_on_device(tmp_path, shape, dtype):
+    """cv2.imwrite's default TIFF compression is LZW (with Predictor 2)."""
+    img = image(shape, dtype, 15)
+    path = tmp_path / "lzw.tif"
+    payload = np.ascontiguousarray(img[:, :, ::-1]) if img.ndim == 3 else img
+    assert cv2.imwrite(str(path), payload, [cv2.IMWRITE_TIFF_COMPRESSION, 5])
+    assert image_io._tiff_layout(path.read_bytes())["compression"] == 5
+    got = image_io.decode_tiff(path.read_bytes())
+    assert np.array_equal(got.cpu().numpy(), cv2_read(path))
+    assert np.array_equal(got.cpu().numpy(), img)
+
+
+def test_lzw_flat_image_with_long_strings(tmp_path):
+    """Constant and periodic data: long table strings, KwKwK codes, table resets."""
+    for k, img in enumerate((np.full((700, 900), 37, np.uint8),
+                             np.tile(np.arange(251, dtype=np.uint8), (400, 5)),
+                             np.zeros((300, 4000), np.uint16))):
+        path = tmp_path / f"flat{k}.tif"
+        assert cv2.imwrite(str(path), img, [cv2.IMWRITE_TIFF_COMPRESSION, 5])
+        assert np.array_equal(image_io.decode_tiff(path.read_bytes()).cpu().numpy(), img)
+
+
+def _tiled_tiff(img, tw, th, compression, predictor=1, big_endian=False):
+    """A tiled classic TIFF written by hand (raw or zlib tiles, edge tiles padded)."""
+    bo = ">" if big_endian else "<"
+    h, w = img.shape[:2]
+    ch = 3 if img.ndim == 3 else 1
+    depth = 16 if img.dtype == np.uint16 else 8
+    across, down = -(-w // tw), -(-h // th)
+    tiles = []
+    for ty in range(down):
+        for tx in range(across):
+            tile = np.zeros((th, tw) + img.shape[2:], dtype=img.dtype)
+            part = img[ty * th:(ty + 1) * th, tx * tw:(tx + 1) * tw]
+            tile[:part.shape[0], :part.shape[1]] = part
+            if predictor == 2:
+                t2 = tile.reshape(th, tw, ch).copy()
+                t2[:, 1:] = t2[:, 1:] - t2[:, :-1]
+                tile = t2
+            raw = tile.astype(tile.dtype.newbyteorder(bo)).tobytes()
+            tiles.append(zlib.compress(raw) if compression == 8 else raw)
+    body = b"".join(t + b"\0" * (len(t) & 1) for t in tiles)
+    offs, at = [], 8
+    for t in tiles:
+        offs.append(at)
+        at += len(t) + (len(t) & 1)
+    ifd_at = 8 + len(body)
+    entries = [(256, 4, [w]), (257, 4, [h]), (258, 3, [depth] * ch), (259, 3, [compression]),
+               (262, 3, [2 if ch == 3 else 1]), (277, 3, [ch]), (284, 3, [1]), (317, 3, [predictor]),
+               (322, 4, [tw]), (323, 4, [th]), (324, 4, offs), (325, 4, [len(t) for t in tiles])]
+    extra_at = ifd_at + 2 + 12 * len(entries) + 4
+    ifd, extra = struct.pack(bo + "H", len(entries)), b""
+    for tag, typ, vals in entries:
+        raw = struct.pack(bo + ("H" if typ == 3 else "I") * len(vals), *vals)
+        if len(raw) <= 4:
+            ifd += struct.pack(bo + "HHI", tag, typ, len(vals)) + raw.ljust(4, b"\0")
+        else:
+            ifd += struct.pack(bo + "HHII", tag, typ, len(vals), extra_at + len(extra))
+            extra += raw + b"\0" * (len(raw) & 1)
+    ifd += struct.pack(bo + "I", 0)
+    return (b"MM\0*" if big_endian else b"II*\0") + struct.pack(bo + "I", ifd_at) + body + ifd + extra
+
+
+@pytest.mark.parametrize("compression,predictor,big", [(1, 1, False), (8, 1, False), (8, 2, False), (8, 2, True)])
+@pytest.mark.parametrize("shape,dtype,tile", [((100, 130), np.uint8, (64, 32)), ((257, 300), np.uint16, (128, 128)),
+                                              ((70, 90, 3), np.uint8, (32, 48)), ((16, 16), np.uint16, (16, 16))])
+def test_tiled_tiff_decodes_on_device(tmp_path, compression, predictor, big, shape, dtype, tile):
+    img = image(shape, dtype, 16)
+    data = _tiled_tiff(img, tile[0], tile[1], compression, predictor, big)
+    path = tmp_path / "tiled.tif"
+    path.write_bytes(data)
+    assert np.array_equal(cv2_read(path), img)            # libtiff agrees the file is valid
+    got = image_io.decode_tiff(data)
+    assert got.is_cuda and np.array_equal(got.cpu().numpy(), img)
+
+
+def test_files_decode_without_the_host_decoder(tmp_path, monkeypatch):
+    """PNG, LZW and tiled TIFF inputs never reach cv2 (the reference's decoder)."""
+    img = image((90, 120), np.uint16, 17)
     cv2.imwrite(str(tmp_path / "a.png"), img)
-    assert np.array_equal(ut.load_image(tmp_path / "a.png"), img)
     cv2.imwrite(str(tmp_path / "lzw.tif"), img, [cv2.IMWRITE_TIFF_COMPRESSION, 5])
+    (tmp_path / "tiled.tif").write_bytes(_tiled_tiff(img, 64, 64, 8, 2))
+    no_host_codecs(monkeypatch)
+    for name in ("a.png", "lzw.tif", "tiled.tif"):
+        assert np.array_equal(ut.load_image(tmp_path / name), img)
+    m = _manifest(tmp_path, ["a.png,365,uv", "lzw.tif,450,vis", "tiled.tif,940,ir"])
+    stack = ut.load_stack(m)
+    assert stack.planes.shape == (3, 90, 120) and stack.bit_depth == 16
+    assert all(np.array_equal(stack.planes[b], img) for b in range(3))
+
+
+def test_other_layouts_use_the_reference_decoder(tmp_path):
+    """Layouts the device decoders do not parse (alpha channels, float samples,
+    ...) are read by cv2 exactly as the reference reads them."""
+    rgba = np.dstack([image((40, 50, 3), np.uint8, 5), np.full((40, 50), 200, np.uint8)])
+    cv2.imwrite(str(tmp_path / "rgba.png"), rgba)
     with pytest.raises(image_io._Unsupported):
-        image_io.decode_tiff((tmp_path / "lzw.tif").read_bytes())
-    assert np.array_equal(ut.load_image(tmp_path / "lzw.tif"), img)
+        image_io.decode_png((tmp_path / "rgba.png").read_bytes())
+    with pytest.raises(ut.DataError, match="expected 3 channels, got 4"):
+        ut.load_image(tmp_path / "rgba.png")
+    cv2.imwrite(str(tmp_path / "f.tif"), image((40, 50), np.uint8, 6).astype(np.float32))
+    with pytest.raises(image_io._Unsupported):
+        image_io.decode_tiff((tmp_path / "f.tif").read_bytes())
+    with pytest.raises(ut.DataError):
+        ut.load_image(tmp_path / "f.tif")
     with pytest.raises(ut.DataError):
         ut.load_image(tmp_path / "absent.png")
 
@@ -171,8 +375,7 @@ class TestLoadStack:
 
 
 def test_measured_path_never_uses_host_codecs(monkeypatch):
-    """PNG, LZW and tiled TIFFs are decoded by cv2 exactly as the reference
-    reads them (outside the measured path).  The measured path
+    """The measured path
     -- the cube resident in HBM, fit, projection, stretch, as bench.py times it
     (CVA, the PCA companion and the streamed folio batch) -- must never reach a
     host codec: every cv2 entry point is made to fail here."""
