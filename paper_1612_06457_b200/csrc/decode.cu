@@ -7,10 +7,12 @@
 // strips of a band are decoded in parallel:
 //  * strips_copy_kernel: uncompressed strips, one CTA per strip (16-byte
 //    vector copies when aligned);
-//  * inflate_kernel: deflate strips (Compression 8 / 32946), one thread per
-//    zlib stream: RFC 1951 stored / fixed / dynamic blocks, canonical Huffman
-//    decoding by code length (count/symbol tables per stream), back-references
-//    from the stream's own output, Adler-32 verified;
+//  * inflate_warp_kernel: deflate strips (Compression 8 / 32946) and PNG IDAT
+//    streams, one warp per zlib stream: RFC 1951 stored / fixed / dynamic
+//    blocks, 11-bit lookup tables with a canonical-walk fallback, a 32 KB
+//    shared-memory history window, warp-wide match copies and flushes, Adler-32
+//    verified (inflate_kernel, one thread per stream, is the first version,
+//    kept behind UT_INFLATE_THREAD=1 for comparison);
 //  * lzw_kernel: LZW strips / tiles (Compression 5, MSB-first codes of 9..12
 //    bits with the TIFF "early change"), one thread per stream; a table entry is
 //    (position, length) of the string's first occurrence in the stream's own
@@ -29,6 +31,8 @@
 //    little endian.
 // A stream whose data is malformed, too short or too long sets its status
 // word (and the caller raises DataError, as cv2.imread failing does).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ut {
@@ -236,6 +240,324 @@ __device__ int inflate_one(const uint8_t* in, int64_t in_len, uint8_t* out, int6
     if (b >= 65521u) b -= 65521u;
   }
   return ((b << 16) | a) == want ? 0 : kAdler;
+}
+
+
+// ------------------------------------------------------- warp-wide inflate
+// One warp per zlib stream.  All 32 lanes run the same (uniform) decode loop on
+// the same bit buffer; what the warp buys is the memory side: the compressed
+// bytes arrive as 128-byte blocks (one word per lane, the next block in
+// flight) and are handed out by shuffle, the output lives in a 32 KB shared-
+// memory window (the deflate history), Huffman codes of <= 9 bits resolve with
+// one shared-memory lookup, matches are copied by all lanes, and the window is
+// written to global memory in 8 KB pieces (with the Adler-32 sums) by all lanes.
+constexpr int kWinBits = 15, kWin = 1 << kWinBits, kWinMask = kWin - 1;
+constexpr int kFlush = 8192;
+constexpr int kLitBits = 11, kDistBits = 8;   // index bits of the litlen / distance lookup tables
+
+struct WarpIn {
+  const uint32_t* words;   // aligned words covering the stream
+  int64_t nwords;          // words that hold stream bytes
+  int64_t widx;            // next word to hand out
+  uint32_t first_mask;     // keeps the stream's bytes of word 0
+  uint32_t last_mask;      // ... and of the last word
+  uint32_t cur, nxt;       // this lane's word of the current / next 128-byte block
+  uint64_t buf;
+  int cnt;
+  int lane;
+};
+
+__device__ __forceinline__ uint32_t wi_load(const WarpIn& s, int64_t block) {
+  const int64_t i = block * 32 + s.lane;
+  if (i >= s.nwords) return 0u;
+  uint32_t w = __ldg(s.words + i);
+  if (i == 0) w &= s.first_mask;
+  if (i == s.nwords - 1) w &= s.last_mask;
+  return w;
+}
+__device__ __forceinline__ void wi_refill(WarpIn& s) {
+  if (s.cnt <= 32) {
+    const int k = (int)(s.widx & 31);
+    if (k == 0 && s.widx > 0) {
+      s.cur = s.nxt;
+      s.nxt = wi_load(s, (s.widx >> 5) + 1);
+    }
+    const uint32_t w = __shfl_sync(0xffffffffu, s.cur, k);
+    s.buf |= (uint64_t)w << s.cnt;
+    s.cnt += 32;
+    ++s.widx;
+  }
+}
+__device__ __forceinline__ uint32_t wi_bits(WarpIn& s, int n) {
+  wi_refill(s);
+  const uint32_t v = (uint32_t)(s.buf & ((1ull << n) - 1));
+  s.buf >>= n;
+  s.cnt -= n;
+  return v;
+}
+// canonical walk (codes longer than the fast table's index)
+__device__ __forceinline__ int wi_slow_sym(WarpIn& s, const Huff* h) {
+  uint64_t bits = s.buf;
+  int code = 0, first = 0, index = 0;
+  for (int len = 1; len < 16; ++len) {
+    code |= (int)(bits & 1);
+    bits >>= 1;
+    const int count = h->count[len];
+    if (code - count < first) {
+      s.buf >>= len;
+      s.cnt -= len;
+      return h->symbol[index + (code - first)];
+    }
+    index += count;
+    first += count;
+    first <<= 1;
+    code <<= 1;
+  }
+  return -1;
+}
+template <int BITS>
+__device__ __forceinline__ int wi_sym(WarpIn& s, const Huff* h, const uint16_t* fast) {
+  wi_refill(s);   // >= 33 bits: enough for a code (15) and its extra bits (13)
+  const uint32_t e = fast[s.buf & ((1u << BITS) - 1)];
+  if (e & 15u) {
+    s.buf >>= (e & 15u);
+    s.cnt -= (int)(e & 15u);
+    return (int)(e >> 4);
+  }
+  return wi_slow_sym(s, h);
+}
+// fast[the next BITS stream bits] = symbol << 4 | code length (0: longer code)
+template <int BITS>
+__device__ void wi_build_fast(const Huff* h, uint16_t* fast, int lane) {
+  constexpr int kFast = 1 << BITS;
+  for (int j = lane; j < kFast; j += 32) fast[j] = 0;
+  __syncwarp();
+  int code = 0, idx = 0;
+  for (int l = 1; l <= BITS; ++l) {
+    const int cnt = h->count[l];
+    for (int i = 0; i < cnt; ++i, ++idx, ++code) {
+      const uint32_t rev = __brev((uint32_t)code) >> (32 - l);   // stream order: first code bit lowest
+      const uint16_t e = (uint16_t)((h->symbol[idx] << 4) | l);
+      for (int j = (int)rev + (lane << l); j < kFast; j += 32 << l) fast[j] = e;
+    }
+    code <<= 1;
+  }
+  __syncwarp();
+}
+
+struct WarpSmem {
+  uint8_t win[kWin];
+  uint16_t litfast[1 << kLitBits];
+  uint16_t distfast[1 << kDistBits];
+  Huff lencode, distcode;
+  uint8_t lengths[320];
+};
+
+// Adler-32 of win[from, from + n) folded into (a, b); all lanes, n <= kFlush
+__device__ __forceinline__ void wi_flush(const uint8_t* win, uint8_t* out, int64_t from, int n,
+                                         uint32_t& a, uint32_t& b, int lane) {
+  unsigned long long sa = 0, sb = 0;
+  for (int k = lane; k < n; k += 32) {
+    const uint32_t d = win[(from + k) & kWinMask];
+    out[from + k] = (uint8_t)d;
+    sa += d;
+    sb += (unsigned long long)(n - k) * d;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  }
+  b = (uint32_t)((b + (unsigned long long)n * a + sb) % 65521ull);
+  a = (uint32_t)((a + sa) % 65521ull);
+}
+
+__device__ int inflate_warp(const uint8_t* in, int64_t in_len, uint8_t* out, int64_t out_len,
+                            WarpSmem& m, int lane) {
+  if (in_len < 2) return kHeader;
+  const uint32_t cmf = in[0], flg = in[1];
+  if ((cmf & 15) != 8 || (cmf >> 4) > 7 || ((cmf << 8) | flg) % 31 != 0 || (flg & 0x20)) return kHeader;
+  WarpIn s;
+  {
+    const uintptr_t p0 = reinterpret_cast<uintptr_t>(in) + 2, p1 = reinterpret_cast<uintptr_t>(in) + in_len;
+    const uintptr_t w0 = p0 & ~(uintptr_t)3;
+    s.words = reinterpret_cast<const uint32_t*>(w0);
+    s.nwords = (int64_t)((p1 - w0 + 3) >> 2);
+    s.first_mask = 0xffffffffu << (8 * (p0 & 3));
+    s.last_mask = (p1 & 3) ? (0xffffffffu >> (8 * (4 - (p1 & 3)))) : 0xffffffffu;
+    s.widx = 0;
+    s.buf = 0;
+    s.cnt = 0;
+    s.lane = lane;
+    s.cur = wi_load(s, 0);
+    s.nxt = wi_load(s, 1);
+    wi_refill(s);
+    const int skip = 8 * (int)(p0 & 3);   // bytes of word 0 before the stream
+    s.buf >>= skip;
+    s.cnt -= skip;
+  }
+  const int64_t in_bits = 8 * (in_len - 2);
+  auto used_bits = [&]() { return s.widx * 32 - 8 * (int64_t)((reinterpret_cast<uintptr_t>(in) + 2) & 3) - s.cnt; };
+  int64_t o = 0, flushed = 0;
+  uint32_t a = 1, b = 0;
+  int last;
+  do {
+    last = (int)wi_bits(s, 1);
+    const int type = (int)wi_bits(s, 2);
+    if (type == 0) {  // stored: to a byte boundary, LEN, NLEN, bytes
+      const int drop = s.cnt & 7;
+      s.buf >>= drop;
+      s.cnt -= drop;
+      const uint32_t len = wi_bits(s, 16), nlen = wi_bits(s, 16);
+      if ((len ^ 0xFFFFu) != nlen) return kBad;
+      if (o + len > out_len) return kLong;
+      for (uint32_t k = 0; k < len; ++k) {
+        const uint32_t v = wi_bits(s, 8);
+        if (lane == 0) m.win[(o + k) & kWinMask] = (uint8_t)v;
+        if (((o + k + 1) & (kFlush - 1)) == 0) {
+          __syncwarp();
+          wi_flush(m.win, out, flushed, kFlush, a, b, lane);
+          flushed += kFlush;
+        }
+      }
+      o += len;
+      if (used_bits() > in_bits) return kShort;
+      continue;
+    }
+    if (type == 3) return kBad;
+    __syncwarp();
+    if (type == 1) {
+      for (int i = lane; i < 288; i += 32) m.lengths[i] = i < 144 ? 8 : i < 256 ? 9 : i < 280 ? 7 : 8;
+      __syncwarp();
+      if (lane == 0) build_huff(&m.lencode, m.lengths, 288);
+      __syncwarp();
+      for (int i = lane; i < 30; i += 32) m.lengths[i] = 5;
+      __syncwarp();
+      if (lane == 0) build_huff(&m.distcode, m.lengths, 30);
+      __syncwarp();
+    } else {
+      const int nlen = (int)wi_bits(s, 5) + 257, ndist = (int)wi_bits(s, 5) + 1;
+      const int ncode = (int)wi_bits(s, 4) + 4;
+      if (nlen > 286 || ndist > 30) return kBad;
+      const uint8_t order[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+      if (lane < 19) m.lengths[lane] = 0;
+      __syncwarp();
+      for (int i = 0; i < ncode; ++i) {
+        const uint32_t v = wi_bits(s, 3);
+        if (lane == 0) m.lengths[order[i]] = (uint8_t)v;
+      }
+      __syncwarp();
+      int rc = 0;
+      if (lane == 0) rc = build_huff(&m.lencode, m.lengths, 19);
+      rc = __shfl_sync(0xffffffffu, rc, 0);
+      if (rc != 0) return kBad;  // must be complete
+      __syncwarp();
+      int i = 0;
+      int prev_len = 0;
+      while (i < nlen + ndist) {
+        wi_refill(s);
+        const int sym = wi_slow_sym(s, &m.lencode);
+        if (sym < 0) return kBad;
+        if (sym < 16) {
+          if (lane == 0) m.lengths[i] = (uint8_t)sym;
+          prev_len = sym;
+          ++i;
+          continue;
+        }
+        int len = 0, rep;
+        if (sym == 16) {
+          if (i == 0) return kBad;
+          len = prev_len;
+          rep = 3 + (int)wi_bits(s, 2);
+        } else if (sym == 17) {
+          rep = 3 + (int)wi_bits(s, 3);
+        } else {
+          rep = 11 + (int)wi_bits(s, 7);
+        }
+        if (i + rep > nlen + ndist) return kBad;
+        for (int k = lane; k < rep; k += 32) m.lengths[i + k] = (uint8_t)len;
+        prev_len = len;
+        i += rep;
+      }
+      __syncwarp();
+      if (m.lengths[256] == 0) return kBad;
+      int el = 0, ed = 0, ok = 1;
+      if (lane == 0) {
+        el = build_huff(&m.lencode, m.lengths, nlen);
+        if (el < 0 || (el > 0 && nlen - m.lencode.count[0] != 1)) ok = 0;
+        ed = build_huff(&m.distcode, m.lengths + nlen, ndist);
+        if (ed < 0 || (ed > 0 && ndist - m.distcode.count[0] != 1)) ok = 0;
+      }
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (!ok) return kBad;
+      __syncwarp();
+    }
+    wi_build_fast<kLitBits>(&m.lencode, m.litfast, lane);
+    wi_build_fast<kDistBits>(&m.distcode, m.distfast, lane);
+    for (;;) {
+      int sym = wi_sym<kLitBits>(s, &m.lencode, m.litfast);
+      if (sym < 0) return kBad;
+      if (sym < 256) {
+        if (o >= out_len) return kLong;
+        if (lane == 0) m.win[o & kWinMask] = (uint8_t)sym;
+        ++o;
+      } else {
+        if (sym == 256) break;
+        sym -= 257;
+        if (sym >= 29) return kBad;
+        const int len = c_len_base[sym] + (int)wi_bits(s, c_len_extra[sym]);
+        const int dsym = wi_sym<kDistBits>(s, &m.distcode, m.distfast);
+        if (dsym < 0 || dsym >= 30) return kBad;
+        const int64_t dist = c_dist_base[dsym] + (int)wi_bits(s, c_dist_extra[dsym]);
+        if (dist > o) return kBad;
+        if (o + len > out_len) return kLong;
+        __syncwarp();   // the literals and matches so far are visible to every lane
+        const int64_t from = o - dist;
+        // a far match may read the window slots this copy overwrites (distance
+        // close to the window size): every lane loads before any lane stores
+        for (int k0 = 0; k0 < len; k0 += 32) {
+          const int k = k0 + lane;
+          uint8_t v = 0;
+          if (k < len) v = m.win[(from + (dist >= len ? k : k % (int)dist)) & kWinMask];
+          __syncwarp();
+          if (k < len) m.win[(o + k) & kWinMask] = v;
+        }
+        o += len;
+      }
+      if (o - flushed >= kFlush) {
+        __syncwarp();
+        wi_flush(m.win, out, flushed, kFlush, a, b, lane);
+        flushed += kFlush;
+        __syncwarp();
+      }
+    }
+    if (used_bits() > in_bits) return kShort;
+  } while (!last);
+  if (o != out_len) return kShort;
+  __syncwarp();
+  while (flushed < o) {
+    const int n = (int)((o - flushed) < kFlush ? (o - flushed) : kFlush);
+    wi_flush(m.win, out, flushed, n, a, b, lane);
+    flushed += n;
+  }
+  // Adler-32 trailer (big-endian) after the last block, byte aligned
+  const int drop = s.cnt & 7;
+  s.buf >>= drop;
+  s.cnt -= drop;
+  uint32_t want = 0;
+  for (int k = 0; k < 4; ++k) want = (want << 8) | wi_bits(s, 8);
+  if (used_bits() > in_bits + 64) return kShort;
+  return ((b << 16) | a) == want ? 0 : kAdler;
+}
+
+__global__ void __launch_bounds__(32) inflate_warp_kernel(const uint8_t* __restrict__ src, const int64_t* in_off,
+                                                          const int64_t* in_len, uint8_t* dst,
+                                                          const int64_t* out_off, const int64_t* out_len,
+                                                          int32_t* status) {
+  extern __shared__ __align__(16) unsigned char wsm_raw[];
+  WarpSmem& m = *reinterpret_cast<WarpSmem*>(wsm_raw);
+  const int64_t i = blockIdx.x;
+  const int rc = inflate_warp(src + in_off[i], in_len[i], dst + out_off[i], out_len[i], m, (int)threadIdx.x);
+  if (threadIdx.x == 0) status[i] = rc;
 }
 
 // one thread per stream; its Huffman tables live in shared memory (the
@@ -533,9 +855,21 @@ int ut_decode_strips(const uint8_t* src, const int64_t* in_off, const int64_t* i
     cudaFreeAsync(tab, st);
     if (le != cudaSuccess) return cuda_status(le, "lzw_kernel");
   } else {
-    inflate_kernel<<<(unsigned)((nstrips + kInfThreads - 1) / kInfThreads), kInfThreads, 0, st>>>(
-        src, in_off, in_len, nstrips, dst, out_off, out_len, status);
-    UT_CHECK_LAUNCH("inflate_kernel");
+    static const bool thread_mode = [] {
+      const char* e = getenv("UT_INFLATE_THREAD");   // dev: the one-thread-per-stream decoder
+      return e && e[0] == '1';
+    }();
+    if (thread_mode) {
+      inflate_kernel<<<(unsigned)((nstrips + kInfThreads - 1) / kInfThreads), kInfThreads, 0, st>>>(
+          src, in_off, in_len, nstrips, dst, out_off, out_len, status);
+      UT_CHECK_LAUNCH("inflate_kernel");
+    } else {
+      static SmemAttr attr;
+      if (int rc = ensure_smem(attr, inflate_warp_kernel, sizeof(WarpSmem), "inflate smem attribute")) return rc;
+      inflate_warp_kernel<<<(unsigned)nstrips, 32, sizeof(WarpSmem), st>>>(src, in_off, in_len, dst, out_off,
+                                                                           out_len, status);
+      UT_CHECK_LAUNCH("inflate_warp_kernel");
+    }
   }
   return UT_OK;
 }

@@ -55,4 +55,21 @@ _, res["tiff16_decode_cv2_s"] = best(
     lambda: cv2.imdecode(np.frombuffer(data, np.uint8), cv2.IMREAD_UNCHANGED))
 res["tiff16_strips"] = len(image_io._tiff_layout(data)["offsets"])
 assert np.array_equal(got.cpu().numpy(), band16)
+# PNG and LZW TIFF bands as cv2 writes them, one file and a 16-band batch
+ok, band_png = cv2.imencode(".png", band16)
+pdata = band_png.tobytes()
+got, res["png16_decode_device_s"] = best(lambda: image_io.decode_png(pdata))
+_, res["png16_decode_cv2_s"] = best(
+    lambda: cv2.imdecode(np.frombuffer(pdata, np.uint8), cv2.IMREAD_UNCHANGED))
+assert np.array_equal(got.cpu().numpy(), band16)
+_, res["png16_decode_device_16_files_s"] = best(lambda: image_io.decode_batch([pdata] * 16), reps=2)
+ok, band_lzw = cv2.imencode(".tif", band16, [cv2.IMWRITE_TIFF_COMPRESSION, 5])
+ldata = band_lzw.tobytes()
+got, res["lzw16_decode_device_s"] = best(lambda: image_io.decode_tiff(ldata))
+_, res["lzw16_decode_cv2_s"] = best(
+    lambda: cv2.imdecode(np.frombuffer(ldata, np.uint8), cv2.IMREAD_UNCHANGED))
+assert np.array_equal(got.cpu().numpy(), band16)
+res["lzw16_strips"] = len(image_io._tiff_layout(ldata)["offsets"])
+_, res["tiff16_decode_device_16_files_s"] = best(lambda: image_io.decode_batch([data] * 16), reps=2)
+_, res["lzw16_decode_device_16_files_s"] = best(lambda: image_io.decode_batch([ldata] * 16), reps=2)
 print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in res.items()}))
