@@ -494,6 +494,19 @@ __device__ int inflate_warp(const uint8_t* in, int64_t in_len, uint8_t* out, int
     wi_build_fast<kLitBits>(&m.lencode, m.litfast, lane);
     wi_build_fast<kDistBits>(&m.distcode, m.distfast, lane);
     for (;;) {
+      {  // literal run: one table lookup per literal up to the next flush boundary
+        const int64_t stop = flushed + kFlush < out_len ? flushed + kFlush : out_len;
+        while (o < stop) {
+          wi_refill(s);
+          const uint32_t e = m.litfast[(uint32_t)s.buf & ((1u << kLitBits) - 1)];
+          const uint32_t l = e & 15u;
+          if (l == 0u || e >= (256u << 4)) break;
+          if (lane == 0) m.win[o & kWinMask] = (uint8_t)(e >> 4);
+          ++o;
+          s.buf >>= l;
+          s.cnt -= (int)l;
+        }
+      }
       int sym = wi_sym<kLitBits>(s, &m.lencode, m.litfast);
       if (sym < 0) return kBad;
       if (sym < 256) {
