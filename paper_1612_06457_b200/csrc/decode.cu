@@ -566,8 +566,7 @@ __global__ void __launch_bounds__(32) inflate_warp_kernel(const uint8_t* __restr
                                                           const int64_t* in_len, uint8_t* dst,
                                                           const int64_t* out_off, const int64_t* out_len,
                                                           int32_t* status) {
-  extern __shared__ __align__(16) unsigned char wsm_raw[];
-  WarpSmem& m = *reinterpret_cast<WarpSmem*>(wsm_raw);
+  __shared__ __align__(16) WarpSmem m;   // 38.6 KB, static: table and window addresses are compile-time offsets
   const int64_t i = blockIdx.x;
   const int rc = inflate_warp(src + in_off[i], in_len[i], dst + out_off[i], out_len[i], m, (int)threadIdx.x);
   if (threadIdx.x == 0) status[i] = rc;
@@ -877,10 +876,8 @@ int ut_decode_strips(const uint8_t* src, const int64_t* in_off, const int64_t* i
           src, in_off, in_len, nstrips, dst, out_off, out_len, status);
       UT_CHECK_LAUNCH("inflate_kernel");
     } else {
-      static SmemAttr attr;
-      if (int rc = ensure_smem(attr, inflate_warp_kernel, sizeof(WarpSmem), "inflate smem attribute")) return rc;
-      inflate_warp_kernel<<<(unsigned)nstrips, 32, sizeof(WarpSmem), st>>>(src, in_off, in_len, dst, out_off,
-                                                                           out_len, status);
+      static_assert(sizeof(WarpSmem) <= 48 * 1024, "inflate window + tables must fit static shared memory");
+      inflate_warp_kernel<<<(unsigned)nstrips, 32, 0, st>>>(src, in_off, in_len, dst, out_off, out_len, status);
       UT_CHECK_LAUNCH("inflate_warp_kernel");
     }
   }
