@@ -495,17 +495,23 @@ __device__ int inflate_warp(const uint8_t* in, int64_t in_len, uint8_t* out, int
     wi_build_fast<kDistBits>(&m.distcode, m.distfast, lane);
     for (;;) {
       {  // literal run: one table lookup per literal up to the next flush boundary
+        // (32-bit counters; every lane stores the same byte, so nothing diverges)
         const int64_t stop = flushed + kFlush < out_len ? flushed + kFlush : out_len;
-        while (o < stop) {
+        uint32_t left = stop > o ? (uint32_t)(stop - o) : 0u;
+        uint32_t pos = (uint32_t)o & kWinMask;
+        const uint32_t left0 = left;
+        while (left) {
           wi_refill(s);
           const uint32_t e = m.litfast[(uint32_t)s.buf & ((1u << kLitBits) - 1)];
           const uint32_t l = e & 15u;
           if (l == 0u || e >= (256u << 4)) break;
-          if (lane == 0) m.win[o & kWinMask] = (uint8_t)(e >> 4);
-          ++o;
+          m.win[pos] = (uint8_t)(e >> 4);
+          pos = (pos + 1u) & kWinMask;
+          --left;
           s.buf >>= l;
           s.cnt -= (int)l;
         }
+        o += left0 - left;
       }
       int sym = wi_sym<kLitBits>(s, &m.lencode, m.litfast);
       if (sym < 0) return kBad;

@@ -659,3 +659,21 @@ def test_class_moments_partition_boundaries(n):
     for got, key in ((sp.within, "within"), (sp.between, "between"),
                      (sp.class_means, "class_means"), (sp.grand_mean, "grand_mean")):
         assert rel_close(got, want[key], 1e-9), key
+
+
+@pytest.mark.parametrize("b,classes,n", [(9, 20, 1000), (32, 17, 4590), (1, 3, 130), (23, 6, 127)])
+def test_class_moments_mixed_chunks(b, classes, n):
+    """Points in caller order (every 128-point chunk holds several classes: one
+    masked tensor-core pass per class present), more than 16 classes (two K1
+    launches), band counts off the 8-row groups."""
+    rng = np.random.default_rng(1000 * b + classes)
+    values = rng.uniform(0.0, 1.0, (b, n)) * rng.uniform(0.5, 2.0, (b, 1))
+    labels = rng.integers(0, classes, n)
+    labels[:classes] = np.arange(classes)   # every class present
+    values += 0.05 * labels[None, :]
+    sp = ut.compute_scatter(dm_of(values, labels))
+    want = oracle.scatter(values, labels)
+    assert np.array_equal(sp.counts, want["counts"])
+    for got, key in ((sp.within, "within"), (sp.between, "between"),
+                     (sp.class_means, "class_means"), (sp.grand_mean, "grand_mean")):
+        assert rel_close(got, want[key], 1e-9), key
