@@ -251,7 +251,9 @@ def _tiff_plan(data: bytes) -> dict:
     are the strips, or the tiles (decoded into a scratch area behind the image
     and scattered into its rows afterwards)."""
     lay = _tiff_layout(data)
-    h, w, ch = int(lay["height"]), int(lay["width"]), int(lay["spp"])
+    h, w, ch = int(lay["height"] or 0), int(lay["width"] or 0), int(lay["spp"])
+    if h <= 0 or w <= 0:
+        raise DataError("TIFF has an empty image")
     depth = int(lay["bps"][0])
     px = ch * depth // 8
     rb = w * px
@@ -270,6 +272,8 @@ def _tiff_plan(data: bytes) -> dict:
         if len(offs) != n or len(counts) != n:
             raise DataError(f"TIFF lists {len(offs)} tiles, expected {n}")
         tile_bytes = th * tw * px
+        if n * tile_bytes > 4 * (h * rb + tile_bytes):
+            raise DataError("TIFF tile size does not fit the image")
         scratch0 = _align(h * rb)
         plan.update(tile_w=tw, tile_h=th, across=across, ntiles=n, scratch=scratch0,
                     out_off=scratch0 + np.arange(n, dtype=np.int64) * tile_bytes,
@@ -277,6 +281,8 @@ def _tiff_plan(data: bytes) -> dict:
                     region=scratch0 + _align(n * tile_bytes))
     else:
         rps = min(int(lay["rps"]), h)
+        if rps <= 0:
+            raise DataError("TIFF RowsPerStrip must be positive")
         n = -(-h // rps)
         offs = np.asarray(lay["offsets"], dtype=np.int64)
         counts = np.asarray(lay["counts"], dtype=np.int64)

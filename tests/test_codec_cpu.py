@@ -119,3 +119,82 @@ def test_tiff_layout_parse():
     assert lay["offsets"] == [8] and lay["counts"] == [img.nbytes]
     with pytest.raises(image_io._Unsupported):
         image_io._tiff_layout(b"\x89PNG\r\n\x1a\n")
+
+
+def _png_bytes(w, h, depth, color, interlace=0, extra=(), idat_parts=2, drop_iend=False):
+    rb = w * {0: 1, 2: 3, 3: 1, 4: 2, 6: 4}[color] * depth // 8
+    raw = b"".join(b"\0" + bytes(rb) for _ in range(h))
+    z = zlib.compress(raw)
+    chunk = lambda k, d: struct.pack(">I", len(d)) + k + d + struct.pack(">I", zlib.crc32(k + d))  # noqa: E731
+    cut = max(1, len(z) // idat_parts)
+    body = b"".join(chunk(b"IDAT", z[i:i + cut]) for i in range(0, len(z), cut))
+    out = b"\x89PNG\r\n\x1a\n" + chunk(b"IHDR", struct.pack(">IIBBBBB", w, h, depth, color, 0, 0, interlace))
+    out += b"".join(chunk(k, d) for k, d in extra) + body
+    return out if drop_iend else out + chunk(b"IEND", b""), z
+
+
+def test_png_plan_host_parsing():
+    """Host chunk walk of the PNG decoder (image_io._png_plan): geometry, the
+    IDAT payloads joined into one zlib stream, and which layouts are left to cv2."""
+    data, z = _png_bytes(7, 5, 16, 2, extra=[(b"tEXt", b"k\0v")], idat_parts=3)
+    plan = image_io._png_plan(data)
+    assert (plan["h"], plan["w"], plan["ch"], plan["depth"]) == (5, 7, 3, 16)
+    assert plan["payload"] == z and plan["code"] == 8
+    assert plan["bytes"] == 5 * 7 * 6 and int(plan["out_len"][0]) == 5 * (7 * 6 + 1)
+    assert int(plan["out_off"][0]) >= plan["bytes"] and plan["region"] >= plan["out_off"][0] + plan["out_len"][0]
+    for kwargs in ({"color": 6}, {"color": 4}, {"color": 3, "extra": [(b"PLTE", bytes(6))]},
+                   {"color": 0, "interlace": 1}, {"color": 0, "extra": [(b"tRNS", b"\0\0")]}):
+        args = {"w": 4, "h": 4, "depth": 8, "color": 0}
+        args.update(kwargs)
+        with pytest.raises(image_io._Unsupported):
+            image_io._png_plan(_png_bytes(**args)[0])
+    with pytest.raises(image_io._Unsupported):
+        image_io._png_plan(b"II*\0" + bytes(16))
+    with pytest.raises(DataError):
+        image_io._png_plan(_png_bytes(4, 4, 8, 0, drop_iend=True)[0])
+    with pytest.raises(DataError):
+        image_io._png_plan(data[:60])
+
+
+def _ifd_tiff(entries, body=b""):
+    ifd_at = 8 + len(body)
+    extra_at = ifd_at + 2 + 12 * len(entries) + 4
+    ifd, extra = struct.pack("<H", len(entries)), b""
+    for tag, typ, vals in entries:
+        raw = struct.pack("<" + ("H" if typ == 3 else "I") * len(vals), *vals)
+        if len(raw) <= 4:
+            ifd += struct.pack("<HHI", tag, typ, len(vals)) + raw.ljust(4, b"\0")
+        else:
+            ifd += struct.pack("<HHII", tag, typ, len(vals), extra_at + len(extra))
+            extra += raw
+    return b"II*\0" + struct.pack("<I", ifd_at) + body + ifd + struct.pack("<I", 0) + extra
+
+
+def test_tiff_plan_tiles_and_lzw():
+    """Host IFD parsing for tiled and LZW TIFFs (image_io._tiff_plan): tiles decode
+    into a scratch area behind the image; degenerate tags are DataErrors."""
+    body = bytes(4 * 16 * 16 * 2)
+    tiled = [(256, 4, [20]), (257, 4, [30]), (258, 3, [16]), (259, 3, [5]), (262, 3, [1]), (277, 3, [1]),
+             (317, 3, [2]), (322, 4, [16]), (323, 4, [16]), (324, 4, [8 + 512 * i for i in range(4)]),
+             (325, 4, [512] * 4)]
+    plan = image_io._tiff_plan(_ifd_tiff(tiled, body))
+    assert plan["tiled"] and plan["code"] == 5 and plan["predictor"] == 2
+    assert (plan["across"], plan["ntiles"], plan["tile_w"], plan["tile_h"]) == (2, 4, 16, 16)
+    assert plan["bytes"] == 30 * 20 * 2 and int(plan["out_off"][0]) == plan["scratch"] >= plan["bytes"]
+    assert list(plan["out_len"]) == [512] * 4 and plan["region"] >= plan["scratch"] + 4 * 512
+    strips = [(256, 4, [20]), (257, 4, [30]), (258, 3, [8]), (259, 3, [5]), (262, 3, [1]), (277, 3, [1]),
+              (273, 4, [8, 208]), (278, 4, [16]), (279, 4, [200, 100])]
+    plan = image_io._tiff_plan(_ifd_tiff(strips, bytes(300)))
+    assert not plan["tiled"] and plan["code"] == 5 and list(plan["out_len"]) == [320, 280]
+    bad = [e if e[0] != 278 else (278, 4, [0]) for e in strips]
+    with pytest.raises(DataError, match="RowsPerStrip"):
+        image_io._tiff_plan(_ifd_tiff(bad, bytes(300)))
+    huge = [e if e[0] not in (322, 323) else (e[0], 4, [1 << 14]) for e in tiled]
+    with pytest.raises(DataError):
+        image_io._tiff_plan(_ifd_tiff(huge, body))
+    past = [e if e[0] != 279 else (279, 4, [200, 5000]) for e in strips]
+    with pytest.raises(DataError, match="past the end"):
+        image_io._tiff_plan(_ifd_tiff(past, bytes(300)))
+    jpeg = [e if e[0] != 259 else (259, 3, [7]) for e in strips]
+    with pytest.raises(image_io._Unsupported):
+        image_io._tiff_plan(_ifd_tiff(jpeg, bytes(300)))
