@@ -23,6 +23,9 @@
 #ifndef UT_PROD_LANES   // project_tma_kernel: the producer warp's lanes share the band copies
 #define UT_PROD_LANES 1     // (cfg 3: K4 0.531 -> 0.443 ms; 0 = one lane issues them all)
 #endif
+#ifndef UT_DMMA_DYNAMIC     // project_dmma_kernel: tiles by global ticket (1) or static round-robin (0)
+#define UT_DMMA_DYNAMIC 1
+#endif
 #ifndef UT_DMMA_PROD_LANES  // project_dmma_kernel: its two producer warps each issue from one
 #define UT_DMMA_PROD_LANES 0  // lane (all lanes measured 0.4% slower on the cfg 4 step)
 #endif
@@ -51,6 +54,7 @@ struct ProjParams {
   int* nonfinite;
   float* part;             // [grid][2 * KG]
   unsigned int* counter;
+  unsigned int* tiles;     // tile tickets of the dynamically scheduled kernels (zero between launches)
 };
 
 template <int BYTES> struct Ld;
@@ -304,7 +308,10 @@ struct Proj {
           p.minmax[p.ktotal + p.k0 + (f - KG)] = r;
         }
       }
-      if (threadIdx.x == 0) *p.counter = 0u;
+      if (threadIdx.x == 0) {
+        *p.counter = 0u;
+        *p.tiles = 0u;   // every CTA has left its tile loop
+      }
     }
   }
 };
@@ -461,9 +468,20 @@ __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, doubl
                : "d"(a), "d"(b));
 }
 
+#ifdef UT_K4_PROBE  // dev builds: %globaltimer at entry / main-loop end of every CTA
+__device__ unsigned long long g_k4_probe[2 * 1024];
+#endif
+
 template <typename T, int KG>
 __global__ void __launch_bounds__(kDmmaCons + 32 * kDmmaProd, 2)
 project_dmma_kernel(ProjParams p) {
+#ifdef UT_K4_PROBE
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_k4_probe[2 * blockIdx.x] = t;
+  }
+#endif
   using Pj = Proj<T, 1, KG, true>;
   __shared__ typename Pj::Smem s;
   extern __shared__ __align__(128) unsigned char dyn[];
@@ -474,11 +492,25 @@ project_dmma_kernel(ProjParams p) {
   T* stages = reinterpret_cast<T*>(dyn);
   uint64_t* full = reinterpret_cast<uint64_t*>(dyn + (size_t)kTmaStages * B * PS * sizeof(T));
   uint64_t* empty = full + kTmaStages;
+#if UT_DMMA_DYNAMIC
+  // Tiles are handed out by a global ticket counter: CTAs on SMs that stream faster
+  // (the per-CTA finish times of the static round-robin spread over 16% under
+  // sustained load, profiles/r2/probes/k4_cta_spread.txt) take more tiles, so all
+  // CTAs finish together.  Producer warp 0 draws the ticket of a stage (the next one
+  // is in flight during the copies) and publishes it; the other producer and the
+  // consumers read it from shared memory.  Scores, min/max (max-merged) and the
+  // NaN flag do not depend on which CTA ran a tile.
+  __shared__ long long tile_of[kTmaStages];
+  __shared__ uint64_t pub[kTmaStages];
+#endif
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < kTmaStages; ++i) {
       mbar_init(&full[i], kDmmaProd);
       mbar_init(&empty[i], kDmmaCons / 32);
+#if UT_DMMA_DYNAMIC
+      mbar_init(&pub[i], 1);
+#endif
     }
     mbar_fence_init();
   }
@@ -510,6 +542,40 @@ project_dmma_kernel(ProjParams p) {
         T* dst = stages + (size_t)st * B * PS;
         const T* src = static_cast<const T*>(p.data) + p0;
         for (int b = pw + kDmmaProd * lane; b < B; b += kDmmaProd * 32)
+          bulk_g2s(dst + (size_t)b * PS, src + (int64_t)b * p.bs, bytes, &full[st], pol);
+      }
+    }
+#elif UT_DMMA_DYNAMIC
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const int nb = B > pw ? (B - 1 - pw) / kDmmaProd + 1 : 0;
+      unsigned int ticket = 0u;
+      if (pw == 0) ticket = atomicAdd(p.tiles, 1u);
+      for (int i = 0;; ++i) {
+        const int st = i % kTmaStages;
+        const uint32_t ph = (uint32_t)(i / kTmaStages) & 1u;
+        int64_t t;
+        if (pw == 0) {
+          if (i >= kTmaStages) mbar_wait(&empty[st], ph ^ 1u);
+          t = (int64_t)ticket < ntiles ? (int64_t)ticket : -1;
+          tile_of[st] = t;
+          mbar_arrive(&pub[st]);
+          if (t >= 0) ticket = atomicAdd(p.tiles, 1u);   // in flight during this tile's copies
+        } else {
+          mbar_wait(&pub[st], ph);
+          t = tile_of[st];
+        }
+        if (t < 0) {   // no tiles left: wake the consumers and stop
+          mbar_arrive(&full[st]);
+          break;
+        }
+        const int64_t p0 = t * kDmmaP;
+        const int64_t npx = (p.npix - p0) < kDmmaP ? (p.npix - p0) : kDmmaP;
+        const uint32_t bytes = (uint32_t)(npx * sizeof(T));
+        mbar_expect_tx(&full[st], bytes * (uint32_t)nb);
+        T* dst = stages + (size_t)st * B * PS;
+        const T* src = static_cast<const T*>(p.data) + p0;
+        for (int b = pw; b < B; b += kDmmaProd)
           bulk_g2s(dst + (size_t)b * PS, src + (int64_t)b * p.bs, bytes, &full[st], pol);
       }
     }
@@ -545,11 +611,20 @@ project_dmma_kernel(ProjParams p) {
     const double bias = am < KG ? (double)s.bias[am] : 0.0;
     const int nq = (B + 3) / 4;
     float lmn = INFINITY, lmx = -INFINITY;  // this lane's component am
+#if UT_DMMA_DYNAMIC && !UT_DMMA_PROD_LANES
+    for (int i = 0;; ++i) {
+      const int st = i % kTmaStages;
+      const uint32_t ph = (uint32_t)(i / kTmaStages) & 1u;
+      mbar_wait(&full[st], ph);
+      const int64_t t = tile_of[st];
+      if (t < 0) break;
+#else
     int i = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
       const int st = i % kTmaStages;
       const uint32_t ph = (uint32_t)(i / kTmaStages) & 1u;
       mbar_wait(&full[st], ph);
+#endif
       const int64_t p0 = t * kDmmaP;
       const int64_t npx = (p.npix - p0) < kDmmaP ? (p.npix - p0) : kDmmaP;
       const T* stage = stages + (size_t)st * B * PS;
@@ -627,6 +702,14 @@ project_dmma_kernel(ProjParams p) {
         mx[k] = lmx;
       }
   }
+#ifdef UT_K4_PROBE
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_k4_probe[2 * blockIdx.x + 1] = t;
+  }
+#endif
   Pj::finish(p, s, mn, mx, chk);
 }
 
@@ -1036,6 +1119,13 @@ using namespace ut;
 
 extern "C" {
 
+#ifdef UT_K4_PROBE
+int ut_debug_k4_probe(unsigned long long* host) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(host, g_k4_probe, sizeof(g_k4_probe)) == cudaSuccess ? 0 : 3;
+}
+#endif
+
 size_t ut_project_ws(void) {
   return 256 + sizeof(float) * (size_t)kMaxGroups * kMaxGrid * (2 * kMaxGroup + 1);
 }
@@ -1079,6 +1169,7 @@ int ut_project_minmax(const ut_cube* cube, const double* coef, int32_t ld_coef,
     p.k0 = k0;
     for (int i = 0; i < kg; ++i) p.comps[i] = components[k0 + i];
     p.counter = reinterpret_cast<unsigned int*>(base) + g;
+    p.tiles = reinterpret_cast<unsigned int*>(base) + 16 + g;
     p.part = reinterpret_cast<float*>(base + 256) + (size_t)g * kMaxGrid * (2 * kMaxGroup + 1);
     const int rc = precision ? launch_prec<true>(p, cube->dtype, kg, vector_ok, st)
                              : launch_prec<false>(p, cube->dtype, kg, vector_ok, st);
