@@ -33,10 +33,6 @@ constexpr int kThreads = N * N;  // 1024 (combine steps use all of them)
 #endif
 constexpr int kTeam = UT_JACOBI_TEAM;  // Jacobi team
 constexpr int kMaxC = 32;        // classes handled by the low-rank path
-#ifndef UT_GJ_WARP
-#define UT_GJ_WARP 1             // low-rank path: register-resident one-warp Gauss-Jordan for C <= kGjC
-#endif
-constexpr int kGjC = 8;
 
 #ifdef UT_PHASES  // dev builds: per-phase %globaltimer stamps of thread 0
 __device__ unsigned long long g_eig_phase[32];
@@ -677,46 +673,6 @@ __device__ bool cva_low_rank_gj(Smem& s, int n, int C, double ridge, int want,
   // [W' | H] is updated in parallel with its own factor m[i][k] / m[k][k];
   // row k is left unnormalized and the pivots are divided out at the end.
   const int wl = n + C;  // columns of [W' | H]
-#if UT_GJ_WARP
-  if (C <= kGjC) {
-    // Few classes (the usual case): the elimination runs on ONE warp out of
-    // registers -- lane i holds row i of [W' | H] (32 + kGjC doubles), the pivot
-    // row arrives by shuffle, no barriers and no shared-memory traffic inside the
-    // 32 steps (14 -> ~4 us at B = 32, C = 6).  Same operations in the same order
-    // as the block version below, so the results are bit-identical.
-    if (tid < 32) {
-      const int lane = tid;
-      double r[N], hr[kGjC], diag = 1.0;
-#pragma unroll
-      for (int q = 0; q < N; ++q) r[q] = (lane < n && q < n) ? s.m[lane * LD + q] : 0.0;
-#pragma unroll
-      for (int c = 0; c < kGjC; ++c) hr[c] = (lane < n && c < C) ? s.h[lane * LD + c] : 0.0;
-      bool ok = true;
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        if (k < n) {  // warp-uniform
-          const double piv = __shfl_sync(0xffffffffu, r[k], k);
-          if (!(piv > 0.0)) ok = false;  // W' not positive definite (uniform)
-          if (lane == k) diag = piv;
-          const double g = (lane == k || lane >= n) ? 0.0 : r[k] * __drcp_rn(piv);
-#pragma unroll
-          for (int q = k + 1; q < N; ++q) r[q] -= g * __shfl_sync(0xffffffffu, r[q], k);
-#pragma unroll
-          for (int c = 0; c < kGjC; ++c) hr[c] -= g * __shfl_sync(0xffffffffu, hr[c], k);
-        }
-      }
-      if (ok && lane < n) {
-#pragma unroll
-        for (int c = 0; c < kGjC; ++c)
-          if (c < C) s.h[lane * LD + c] = hr[c] / diag;
-      }
-      if (lane == 0) s.flag = ok ? 1 : 0;
-    }
-    __syncthreads();
-    if (!s.flag) return false;
-  } else
-#endif
-  {
   for (int k = 0; k < n; ++k) {
     const double piv = s.m[k * LD + k];
     if (!(piv > 0.0)) {  // uniform: W' not positive definite
@@ -743,7 +699,6 @@ __device__ bool cva_low_rank_gj(Smem& s, int n, int C, double ridge, int want,
   if (tid == 0) s.flag = 1;
   __syncthreads();
   if (!s.flag) return false;
-  }
   EPH(6);
   // now s.h = X = W'^-1 H.  T = H^T X (H from the outputs), symmetrized
   for (int e = tid; e < C * C; e += nt) {
