@@ -848,9 +848,11 @@ region_imma_kernel(ImParams r) {
             for (int p = 0; p < 16; ++p) {
               const double xw = im_widen(x[p]);
               const double t = fma(xw, scale, addend);
+#if !(defined(UT_IM_PROBE) && (UT_IM_PROBE & 4))   // dev probe 4: no range check, no sample sums
               bad |= (uint32_t)__double2hiint(t) ^ 0x43380000u;
-              wd[p] = (uint32_t)__double2loint(t);
               dsum[p % UT_IM_DSUM] += xw;
+#endif
+              wd[p] = (uint32_t)__double2loint(t);
             }
           } else {
 #pragma unroll
