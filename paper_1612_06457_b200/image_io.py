@@ -311,7 +311,13 @@ def _png_plan(data: bytes) -> dict:
         body_at = at + 8
         if body_at + n + 4 > len(data):
             raise DataError("PNG chunk runs past the end of the file")
+        if kind in (b"IHDR", b"IDAT"):   # critical chunks: CRC checked, as libpng does
+            (crc,) = struct.unpack(">I", data[body_at + n:body_at + n + 4])
+            if zlib.crc32(data[at + 4:body_at + n]) != crc:
+                raise DataError(f"PNG {kind.decode()} chunk fails its CRC")
         if kind == b"IHDR":
+            if n != 13:
+                raise DataError("PNG IHDR chunk has the wrong length")
             ihdr = struct.unpack(">IIBBBBB", data[body_at:body_at + 13])
         elif kind == b"IDAT":
             idat.append(data[body_at:body_at + n])

@@ -154,6 +154,10 @@ def test_png_plan_host_parsing():
         image_io._png_plan(_png_bytes(4, 4, 8, 0, drop_iend=True)[0])
     with pytest.raises(DataError):
         image_io._png_plan(data[:60])
+    bad = bytearray(data)
+    bad[bad.index(b"IDAT") + 6] ^= 0x40          # payload bit flip: the chunk CRC catches it
+    with pytest.raises(DataError, match="CRC"):
+        image_io._png_plan(bytes(bad))
 
 
 def _ifd_tiff(entries, body=b""):

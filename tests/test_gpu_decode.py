@@ -207,7 +207,11 @@ def test_corrupt_png_raises():
     data = bytearray(_png_file(img, [4]))
     at = data.index(b"IDAT") + 4
     data[at + 20:at + 50] = bytes(30)
-    with pytest.raises(ut.DataError):
+    with pytest.raises(ut.DataError, match="CRC"):        # the host's chunk check
+        image_io.decode_png(bytes(data))
+    (n,) = struct.unpack(">I", data[at - 8:at - 4])        # same damage under a valid CRC:
+    data[at + n:at + n + 4] = struct.pack(">I", zlib.crc32(bytes(data[at - 4:at + n])))
+    with pytest.raises(ut.DataError, match="undecodable"):  # the device's inflate / Adler-32 check
         image_io.decode_png(bytes(data))
     good = _png_file(img, [0])                     # the same image with a filter byte of 7
     rows = bytearray(_png_filter_rows(img, [0]))
