@@ -495,21 +495,42 @@ __device__ int inflate_warp(const uint8_t* in, int64_t in_len, uint8_t* out, int
     wi_build_fast<kDistBits>(&m.distcode, m.distfast, lane);
     for (;;) {
       {  // literal run: one table lookup per literal up to the next flush boundary
-        // (32-bit counters; every lane stores the same byte, so nothing diverges)
+        // (32-bit counters; every lane stores the same byte, so nothing diverges).
+        // ncu of a PNG stream: the loop is bound by its taken branches and by the
+        // shared-window base ptxas rebuilds (S2UR -> ULEA) in front of every lookup,
+        // so three literals are decoded per refill check -- after a refill the
+        // buffer holds >= 33 bits = three table codes of <= 11 bits -- and the table
+        // / window addresses live in registers the compiler cannot see through.
         const int64_t stop = flushed + kFlush < out_len ? flushed + kFlush : out_len;
         uint32_t left = stop > o ? (uint32_t)(stop - o) : 0u;
         uint32_t pos = (uint32_t)o & kWinMask;
         const uint32_t left0 = left;
-        while (left) {
-          wi_refill(s);
-          const uint32_t e = m.litfast[(uint32_t)s.buf & ((1u << kLitBits) - 1)];
-          const uint32_t l = e & 15u;
-          if (l == 0u || e >= (256u << 4)) break;
-          m.win[pos] = (uint8_t)(e >> 4);
+        uint32_t lit_at, win_at;
+        asm volatile("mov.u32 %0, %1;" : "=r"(lit_at) : "r"(smem_u32(m.litfast)));
+        asm volatile("mov.u32 %0, %1;" : "=r"(win_at) : "r"(smem_u32(m.win)));
+        auto literal = [&]() -> bool {   // one table literal, or false (other symbol / long code)
+          uint16_t e16;
+          asm volatile("ld.shared.u16 %0, [%1];"
+                       : "=h"(e16)
+                       : "r"(lit_at + (((uint32_t)s.buf & ((1u << kLitBits) - 1)) << 1)));
+          const uint32_t e = e16, l = e & 15u;
+          if (l == 0u || e >= (256u << 4)) return false;
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(win_at + pos), "r"(e >> 4) : "memory");
           pos = (pos + 1u) & kWinMask;
           --left;
           s.buf >>= l;
           s.cnt -= (int)l;
+          return true;
+        };
+        while (left >= 3u) {
+          wi_refill(s);
+          if (!literal()) break;
+          if (!literal()) break;
+          if (!literal()) break;
+        }
+        while (left) {
+          wi_refill(s);
+          if (!literal()) break;
         }
         o += left0 - left;
       }
