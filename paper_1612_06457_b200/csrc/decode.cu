@@ -738,20 +738,16 @@ __device__ __forceinline__ uint32_t paeth(uint32_t a, uint32_t b, uint32_t c) {
   return (pa <= pb && pa <= pc) ? a : (pb <= pc ? b : c);
 }
 
-// table row i: work_off, out_off, rows, cols, channels, depth.  work holds the
-// inflated scanlines ([filter byte][row bytes] per row); they are reconstructed
-// in place.  One warp per image.
-__global__ void __launch_bounds__(32) png_unfilter_kernel(uint8_t* __restrict__ work,
-                                                          const int64_t* __restrict__ table,
-                                                          int32_t* __restrict__ status) {
-  __shared__ uint8_t sin[2][33][kPngCx * kPngMaxBpp];   // row 32 = the row above the group
-  __shared__ uint8_t sout[2][32][kPngCx * kPngMaxBpp];
-  const int64_t* tb = table + (int64_t)blockIdx.x * 6;
-  const int64_t rows = tb[2], cols = tb[3];
-  const int bpp = (int)(tb[4] * tb[5] / 8);
-  const int64_t rb = cols * bpp, stride = rb + 1;
-  uint8_t* base = work + tb[0];
-  const int lane = threadIdx.x;
+// One image, BPP bytes per pixel (1: gray 8, 2: gray 16, 3: RGB 8, 6: RGB 16).  work holds
+// the inflated scanlines ([filter byte][row bytes] per row); they are reconstructed
+// in place by one warp.
+template <int BPP>
+__device__ int png_unfilter_image(uint8_t* __restrict__ base, int64_t rows, int64_t cols,
+                                  uint8_t (*sin)[33][kPngCx * kPngMaxBpp],
+                                  uint8_t (*sout)[32][kPngCx * kPngMaxBpp], int lane) {
+  constexpr int CB = kPngCx * BPP;           // bytes of a full chunk row
+  constexpr int IT = (CB + 31) / 32;         // byte loads per lane and row
+  const int64_t rb = cols * BPP, stride = rb + 1;
   const int64_t nchunks = (cols + kPngCx - 1) / kPngCx;
   int bad = 0;
   for (int64_t y0 = 0; y0 < rows; y0 += 32) {
@@ -759,27 +755,46 @@ __global__ void __launch_bounds__(32) png_unfilter_kernel(uint8_t* __restrict__ 
     const bool live = y < rows;
     const int ft = live ? base[y * stride] : 0;
     if (ft > 4) bad = 1;
-    uint32_t a[kPngMaxBpp], b[kPngMaxBpp], c[kPngMaxBpp];
+    uint32_t a[BPP], b[BPP], c[BPP];
 #pragma unroll
-    for (int j = 0; j < kPngMaxBpp; ++j) a[j] = b[j] = c[j] = 0;
-    auto load_chunk = [&](int64_t k) {   // filtered bytes of chunk k of the 32 rows + the row above
+    for (int j = 0; j < BPP; ++j) a[j] = b[j] = c[j] = 0;
+    // filtered bytes of chunk k of the 32 rows + the row above: four rows' loads are
+    // issued together (one memory latency per four rows, not per row)
+    auto load_chunk = [&](int64_t k) {
       const int buf = (int)(k & 1);
-      const int64_t c0 = k * kPngCx * bpp;
-      const int nb = (int)((rb - c0) < (int64_t)kPngCx * bpp ? (rb - c0) : (int64_t)kPngCx * bpp);
-      for (int r = 0; r < 33; ++r) {
-        const int64_t yy = r < 32 ? y0 + r : y0 - 1;
-        if (yy < 0 || yy >= rows) {
-          if (r == 32) for (int e = lane; e < nb; e += 32) sin[buf][r][e] = 0;
-          continue;
+      const int64_t c0 = k * CB;
+      const int nb = (int)((rb - c0) < (int64_t)CB ? (rb - c0) : (int64_t)CB);
+      for (int r0 = 0; r0 < 33; r0 += 4) {
+        uint8_t v[4][IT];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = r0 + q;
+          const int64_t yy = r < 32 ? y0 + r : y0 - 1;
+          const bool ok = r < 33 && yy >= 0 && yy < rows;
+          const uint8_t* src = base + (ok ? yy : 0) * stride + 1 + c0;
+#pragma unroll
+          for (int it = 0; it < IT; ++it) {
+            const int e = it * 32 + lane;
+            v[q][it] = (ok && e < nb) ? src[e] : (uint8_t)0;
+          }
         }
-        const uint8_t* src = base + yy * stride + 1 + c0;
-        for (int e = lane; e < nb; e += 32) sin[buf][r][e] = src[e];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = r0 + q;
+          if (r < 33) {
+#pragma unroll
+            for (int it = 0; it < IT; ++it) {
+              const int e = it * 32 + lane;
+              if (e < CB) sin[buf][r][e] = v[q][it];
+            }
+          }
+        }
       }
     };
     auto flush_chunk = [&](int64_t k) {  // reconstructed bytes of chunk k back in place
       const int buf = (int)(k & 1);
-      const int64_t c0 = k * kPngCx * bpp;
-      const int nb = (int)((rb - c0) < (int64_t)kPngCx * bpp ? (rb - c0) : (int64_t)kPngCx * bpp);
+      const int64_t c0 = k * CB;
+      const int nb = (int)((rb - c0) < (int64_t)CB ? (rb - c0) : (int64_t)CB);
       for (int r = 0; r < 32 && y0 + r < rows; ++r) {
         uint8_t* dst = base + (y0 + r) * stride + 1 + c0;
         for (int e = lane; e < nb; e += 32) dst[e] = sout[buf][r][e];
@@ -795,27 +810,25 @@ __global__ void __launch_bounds__(32) png_unfilter_kernel(uint8_t* __restrict__ 
         __syncwarp();
       }
       // the pixel lane - 1 produced last step is this lane's "up" pixel
-      uint32_t up[kPngMaxBpp];
+      uint32_t up[BPP];
 #pragma unroll
-      for (int j = 0; j < kPngMaxBpp; ++j) up[j] = __shfl_up_sync(0xffffffffu, a[j], 1);
+      for (int j = 0; j < BPP; ++j) up[j] = __shfl_up_sync(0xffffffffu, a[j], 1);
       const int64_t x = s - lane;
       if (live && x >= 0 && x < cols) {
         const int buf = (int)((x / kPngCx) & 1);
-        const int xc = (int)(x % kPngCx) * bpp;
+        const int xc = (int)(x % kPngCx) * BPP;
 #pragma unroll
-        for (int j = 0; j < kPngMaxBpp; ++j) {
-          if (j < bpp) {
-            c[j] = x == 0 ? 0u : b[j];
-            b[j] = lane == 0 ? (uint32_t)sin[buf][32][xc + j] : up[j];
-            const uint32_t left = x == 0 ? 0u : a[j];
-            uint32_t pred = 0;
-            if (ft == 1) pred = left;
-            else if (ft == 2) pred = b[j];
-            else if (ft == 3) pred = (left + b[j]) >> 1;
-            else if (ft == 4) pred = paeth(left, b[j], c[j]);
-            a[j] = ((uint32_t)sin[buf][lane][xc + j] + pred) & 0xffu;
-            sout[buf][lane][xc + j] = (uint8_t)a[j];
-          }
+        for (int j = 0; j < BPP; ++j) {
+          c[j] = x == 0 ? 0u : b[j];
+          b[j] = lane == 0 ? (uint32_t)sin[buf][32][xc + j] : up[j];
+          const uint32_t left = x == 0 ? 0u : a[j];
+          uint32_t pred = 0;
+          if (ft == 1) pred = left;
+          else if (ft == 2) pred = b[j];
+          else if (ft == 3) pred = (left + b[j]) >> 1;
+          else if (ft == 4) pred = paeth(left, b[j], c[j]);
+          a[j] = ((uint32_t)sin[buf][lane][xc + j] + pred) & 0xffu;
+          sout[buf][lane][xc + j] = (uint8_t)a[j];
         }
       }
     }
@@ -825,7 +838,28 @@ __global__ void __launch_bounds__(32) png_unfilter_kernel(uint8_t* __restrict__ 
     __syncwarp();
     __threadfence_block();
   }
-  bad = __any_sync(0xffffffffu, bad);
+  return __any_sync(0xffffffffu, bad);
+}
+
+// table row i: work_off, out_off, rows, cols, channels, depth.  One warp per image.
+__global__ void __launch_bounds__(32) png_unfilter_kernel(uint8_t* __restrict__ work,
+                                                          const int64_t* __restrict__ table,
+                                                          int32_t* __restrict__ status) {
+  __shared__ uint8_t sin[2][33][kPngCx * kPngMaxBpp];   // row 32 = the row above the group
+  __shared__ uint8_t sout[2][32][kPngCx * kPngMaxBpp];
+  const int64_t* tb = table + (int64_t)blockIdx.x * 6;
+  const int64_t rows = tb[2], cols = tb[3];
+  const int bpp = (int)(tb[4] * tb[5] / 8);
+  uint8_t* base = work + tb[0];
+  const int lane = threadIdx.x;
+  int bad;
+  switch (bpp) {
+    case 1: bad = png_unfilter_image<1>(base, rows, cols, sin, sout, lane); break;
+    case 2: bad = png_unfilter_image<2>(base, rows, cols, sin, sout, lane); break;
+    case 3: bad = png_unfilter_image<3>(base, rows, cols, sin, sout, lane); break;
+    case 6: bad = png_unfilter_image<6>(base, rows, cols, sin, sout, lane); break;
+    default: bad = 1; break;
+  }
   if (lane == 0) status[blockIdx.x] = bad ? kBad : 0;
 }
 
