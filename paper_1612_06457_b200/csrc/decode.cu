@@ -345,10 +345,30 @@ __device__ void wi_build_fast(const Huff* h, uint16_t* fast, int lane) {
   __syncwarp();
 }
 
+// lit2[next kLitBits stream bits] = bits consumed | count << 5 | first literal << 8 |
+// second literal << 16: the literal the bits start with and, if its code leaves room
+// for another complete literal code, that one too (count 1 or 2); 0 if the bits start
+// with a length / end-of-block symbol or a code longer than the table index.
+__device__ void wi_build_lit2(const uint16_t* fast, uint32_t* lit2, int lane) {
+  constexpr int kFast = 1 << kLitBits;
+  for (int i = lane; i < kFast; i += 32) {
+    const uint32_t e1 = fast[i], l1 = e1 & 15u, s1 = e1 >> 4;
+    uint32_t v = 0u;
+    if (l1 != 0u && s1 < 256u) {
+      v = l1 | (1u << 5) | (s1 << 8);
+      const uint32_t e2 = fast[(uint32_t)i >> l1], l2 = e2 & 15u, s2 = e2 >> 4;   // high bits read as 0
+      if (l2 != 0u && l1 + l2 <= (uint32_t)kLitBits && s2 < 256u) v = (l1 + l2) | (2u << 5) | (s1 << 8) | (s2 << 16);
+    }
+    lit2[i] = v;
+  }
+  __syncwarp();
+}
+
 struct WarpSmem {
   uint8_t win[kWin];
   uint16_t litfast[1 << kLitBits];
   uint16_t distfast[1 << kDistBits];
+  uint32_t lit2[1 << kLitBits];   // one or two literals per lookup (see wi_build_lit2)
   Huff lencode, distcode;
   uint8_t lengths[320];
 };
@@ -493,6 +513,7 @@ __device__ int inflate_warp(const uint8_t* in, int64_t in_len, uint8_t* out, int
     }
     wi_build_fast<kLitBits>(&m.lencode, m.litfast, lane);
     wi_build_fast<kDistBits>(&m.distcode, m.distfast, lane);
+    wi_build_lit2(m.litfast, m.lit2, lane);
     for (;;) {
       {  // literal run: one table lookup per literal up to the next flush boundary
         // (32-bit counters; every lane stores the same byte, so nothing diverges).
@@ -506,29 +527,38 @@ __device__ int inflate_warp(const uint8_t* in, int64_t in_len, uint8_t* out, int
         uint32_t pos = (uint32_t)o & kWinMask;
         const uint32_t left0 = left;
         uint32_t lit_at, win_at;
-        asm volatile("mov.u32 %0, %1;" : "=r"(lit_at) : "r"(smem_u32(m.litfast)));
+        asm volatile("mov.u32 %0, %1;" : "=r"(lit_at) : "r"(smem_u32(m.lit2)));
         asm volatile("mov.u32 %0, %1;" : "=r"(win_at) : "r"(smem_u32(m.win)));
-        auto literal = [&]() -> bool {   // one table literal, or false (other symbol / long code)
-          uint16_t e16;
-          asm volatile("ld.shared.u16 %0, [%1];"
-                       : "=h"(e16)
-                       : "r"(lit_at + (((uint32_t)s.buf & ((1u << kLitBits) - 1)) << 1)));
-          const uint32_t e = e16, l = e & 15u;
-          if (l == 0u || e >= (256u << 4)) return false;
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(win_at + pos), "r"(e >> 4) : "memory");
+        // one lookup = one or two literals (<= kLitBits bits), or false (other symbol / long code)
+        auto literal = [&]() -> bool {
+          uint32_t e;
+          asm volatile("ld.shared.u32 %0, [%1];"
+                       : "=r"(e)
+                       : "r"(lit_at + (((uint32_t)s.buf & ((1u << kLitBits) - 1)) << 2)));
+          const uint32_t n = (e >> 5) & 3u, l = e & 31u;
+          if (n == 0u) return false;
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(win_at + pos), "r"((e >> 8) & 0xffu) : "memory");
           pos = (pos + 1u) & kWinMask;
-          --left;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "setp.eq.u32 p, %2, 2;\n\t"
+              "@p st.shared.u8 [%0], %1;\n\t"
+              "}" ::"r"(win_at + pos),
+              "r"(e >> 16), "r"(n)
+              : "memory");
+          pos = (pos + n - 1u) & kWinMask;
+          left -= n;
           s.buf >>= l;
           s.cnt -= (int)l;
           return true;
         };
-        while (left >= 3u) {
+        while (left >= 6u) {   // three lookups (<= 33 bits, <= 6 literals) per refill check
           wi_refill(s);
           if (!literal()) break;
           if (!literal()) break;
           if (!literal()) break;
         }
-        while (left) {
+        while (left >= 2u) {
           wi_refill(s);
           if (!literal()) break;
         }
