@@ -70,6 +70,14 @@ _, res["lzw16_decode_cv2_s"] = best(
     lambda: cv2.imdecode(np.frombuffer(ldata, np.uint8), cv2.IMREAD_UNCHANGED))
 assert np.array_equal(got.cpu().numpy(), band16)
 res["lzw16_strips"] = len(image_io._tiff_layout(ldata)["offsets"])
+# the 8-bit code plane (compressible: match-heavy streams), as cv2 and as the device write it
+c8 = ref_png.tobytes()
+got, res["png8_cv2file_decode_device_s"] = best(lambda: image_io.decode_png(c8))
+assert np.array_equal(got.cpu().numpy(), code8)
+_, res["png8_cv2file_decode_cv2_s"] = best(
+    lambda: cv2.imdecode(np.frombuffer(c8, np.uint8), cv2.IMREAD_UNCHANGED))
+got, res["png8_devfile_decode_device_s"] = best(lambda: image_io.decode_png(png))
+assert np.array_equal(got.cpu().numpy(), code8)
 _, res["tiff16_decode_device_16_files_s"] = best(lambda: image_io.decode_batch([data] * 16), reps=2)
 _, res["lzw16_decode_device_16_files_s"] = best(lambda: image_io.decode_batch([ldata] * 16), reps=2)
 print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in res.items()}))
