@@ -633,9 +633,20 @@ __device__ __forceinline__ void transpose4(uint32_t a, uint32_t b, uint32_t c, u
   out[3] = __byte_perm(t1, t3, 0x7632);
 }
 
+#ifdef UT_K2_PROBE  // dev builds: %globaltimer at entry / exit of every CTA
+__device__ unsigned long long g_k2_probe[2 * 160];
+#endif
+
 template <typename T>
 __global__ void __launch_bounds__(kImThreads, 1)
 region_imma_kernel(ImParams r) {
+#ifdef UT_K2_PROBE
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_k2_probe[2 * blockIdx.x] = t;
+  }
+#endif
   extern __shared__ __align__(128) unsigned char dyn_im[];
   constexpr int PS = im_ps<T>();
   const int B = r.bands;
@@ -900,6 +911,13 @@ region_imma_kernel(ImParams r) {
   }
   tc_fence_before();
   __syncthreads();
+#ifdef UT_K2_PROBE
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_k2_probe[2 * blockIdx.x + 1] = t;
+  }
+#endif
   if (tid == 0 && bad_any) atomicOr(r.flag, 1);
   if (tid < kMaxBands) {  // fixed order over the converter warps
     double v = 0.0;
@@ -1090,6 +1108,13 @@ thread_local int g_region_path = -1;  // path of this thread's last ut_region_mo
 }
 
 extern "C" {
+
+#ifdef UT_K2_PROBE
+int ut_debug_k2_probe(unsigned long long* host) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(host, g_k2_probe, sizeof(g_k2_probe)) == cudaSuccess ? 0 : 3;
+}
+#endif
 
 int32_t ut_region_last_path(void) { return g_region_path; }
 
