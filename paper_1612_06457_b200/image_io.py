@@ -71,8 +71,27 @@ def _chunk(kind: bytes, data: bytes) -> bytes:
     return struct.pack(">I", len(data)) + kind + data + struct.pack(">I", zlib.crc32(kind + data))
 
 
-def encode_png(img) -> bytes:
-    """PNG file bytes of a code image (device or host array)."""
+class PendingEncode:
+    """An encode enqueued on the device: ``parts()`` waits for it and returns the
+    file's byte pieces (host), so a caller can keep several images in flight and
+    write finished files while the next ones encode."""
+
+    def __init__(self, finish):
+        self._finish = finish
+        self._parts = None
+
+    def parts(self) -> list:
+        if self._parts is None:
+            self._parts = self._finish()
+            self._finish = None
+        return self._parts
+
+    def bytes(self) -> bytes:
+        return b"".join(bytes(p) for p in self.parts())
+
+
+def encode_png_start(img) -> PendingEncode:
+    """Enqueue the PNG encode of a code image (device or host array)."""
     t, depth, ch = _image_on_device(img)
     rows, cols = int(t.shape[0]), int(t.shape[1])
     L = _lib.lib()
@@ -84,19 +103,32 @@ def encode_png(img) -> bytes:
         _lib.check(L.ut_encode_png(t.data_ptr(), rows, cols, ch, depth, out.data_ptr(), cap,
                                    n.data_ptr(), ws.data_ptr(), ws.numel(), dev.stream_handle()),
                    "ut_encode_png")
-        idat = out[: int(n.item())].cpu().numpy().tobytes()
+        done = torch.cuda.Event()
+        done.record()
     ihdr = struct.pack(">IIBBBBB", cols, rows, depth, 2 if ch == 3 else 0, 0, 0, 0)
-    return _PNG_SIGNATURE + _chunk(b"IHDR", ihdr) + idat + _chunk(b"IEND", b"")
+
+    def finish():   # may run on another thread: wait for the encode, then read back
+        done.synchronize()
+        with torch.cuda.device(out.device):
+            idat = out[: int(n.item())].cpu().numpy()
+        return [_PNG_SIGNATURE + _chunk(b"IHDR", ihdr), memoryview(idat), _chunk(b"IEND", b"")]
+
+    return PendingEncode(finish)
+
+
+def encode_png(img) -> bytes:
+    """PNG file bytes of a code image (device or host array)."""
+    return encode_png_start(img).bytes()
 
 
 def _rows_per_strip(rows: int, row_bytes: int) -> int:
     return max(1, min(rows, _STRIP_TARGET // max(1, row_bytes)))
 
 
-def encode_tiff(img, compression: str = "none") -> bytes:
-    """Baseline little-endian TIFF of a code image: one IFD, strips of about
-    256 KB, compression 1 (raw) or 8 (zlib deflate with horizontal
-    differencing, Predictor 2)."""
+def encode_tiff_start(img, compression: str = "none") -> PendingEncode:
+    """Enqueue the TIFF encode of a code image: one IFD, strips of about 256 KB,
+    compression 1 (raw) or 8 (zlib deflate with horizontal differencing,
+    Predictor 2)."""
     if compression not in _TIFF_COMPRESSION:
         raise DataError(f"TIFF compression must be 'none' or 'deflate', got {compression!r}")
     code = _TIFF_COMPRESSION[compression]
@@ -116,9 +148,22 @@ def encode_tiff(img, compression: str = "none") -> bytes:
         _lib.check(L.ut_encode_tiff(t.data_ptr(), rows, cols, ch, depth, code, rps, out.data_ptr(),
                                     cap, sizes.data_ptr(), n.data_ptr(), ws.data_ptr(),
                                     ws.numel(), dev.stream_handle()), "ut_encode_tiff")
-        body = out[: int(n.item())].cpu().numpy().tobytes()
-        strip_bytes = sizes.cpu().numpy().astype(np.int64)
-    return _tiff_file(body, strip_bytes, rows, cols, ch, depth, code, rps)
+        done = torch.cuda.Event()
+        done.record()
+
+    def finish():   # may run on another thread: wait for the encode, then read back
+        done.synchronize()
+        with torch.cuda.device(out.device):
+            body = out[: int(n.item())].cpu().numpy().tobytes()
+            strip_bytes = sizes.cpu().numpy().astype(np.int64)
+        return [_tiff_file(body, strip_bytes, rows, cols, ch, depth, code, rps)]
+
+    return PendingEncode(finish)
+
+
+def encode_tiff(img, compression: str = "none") -> bytes:
+    """Baseline little-endian TIFF of a code image (see encode_tiff_start)."""
+    return encode_tiff_start(img, compression).bytes()
 
 
 def _tiff_file(body: bytes, strip_bytes, rows, cols, ch, depth, code, rps) -> bytes:
@@ -164,27 +209,40 @@ def _tiff_file(body: bytes, strip_bytes, rows, cols, ch, depth, code, rps) -> by
     return header + body + pad + ifd + extra
 
 
-def save_image(img, path: str | Path, compression: str = "none") -> None:
-    """Write a grayscale or RGB code image as TIFF or PNG (rendering.py:303-331).
-
-    ``img`` may be a host array or a device tensor (e.g. rendered codes still
-    in HBM); the encode runs on the device either way."""
+def save_image_start(img, path: str | Path, compression: str = "none"):
+    """Check the arguments of save_image and enqueue the encode; returns a
+    function that waits for the device and writes the file."""
     path = Path(path)
     check_image(img)
     suffix = path.suffix.lower()
     if suffix in (".tif", ".tiff"):
         if compression not in _TIFF_COMPRESSION:
             raise DataError(f"TIFF compression must be 'none' or 'deflate', got {compression!r}")
-        data = encode_tiff(img, compression)
+        pending = encode_tiff_start(img, compression)
     elif suffix == ".png":
-        data = encode_png(img)
+        pending = encode_png_start(img)
     else:
         raise DataError(f"unsupported image format {suffix!r} (use .tif/.tiff/.png)")
-    path.parent.mkdir(parents=True, exist_ok=True)
-    try:
-        path.write_bytes(data)
-    except OSError as e:
-        raise DataError(f"failed to write image {path}: {e}") from None
+
+    def write():
+        parts = pending.parts()
+        path.parent.mkdir(parents=True, exist_ok=True)
+        try:
+            with open(path, "wb") as f:
+                for part in parts:
+                    f.write(part)
+        except OSError as e:
+            raise DataError(f"failed to write image {path}: {e}") from None
+
+    return write
+
+
+def save_image(img, path: str | Path, compression: str = "none") -> None:
+    """Write a grayscale or RGB code image as TIFF or PNG (rendering.py:303-331).
+
+    ``img`` may be a host array or a device tensor (e.g. rendered codes still
+    in HBM); the encode runs on the device either way."""
+    save_image_start(img, path, compression)()
 
 
 # ------------------------------------------------------------------ decode

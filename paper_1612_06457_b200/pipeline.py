@@ -407,6 +407,8 @@ class FolioStream:
 # HBM; fewer otherwise.  The reference batches 8 planes at a time to bound host
 # memory (pipeline.py:44), re-reading the cube once per batch.
 _RENDER_BATCH = 32
+_ENCODES_IN_FLIGHT = 4   # planes encoding on the device while earlier files are written
+_WRITERS = 4             # host threads waiting on finished encodes and writing files
 
 
 def _render_batch(ds, n_specs: int, depth_bytes: int = 2) -> int:
@@ -443,9 +445,14 @@ def render_planes(stack, model: ProjectionModel, specs: list[RenderSpec], out_di
     in HBM), each spec renders codes on the device (full range from the
     projector's min/max, training range, percentile select), compose_rgb
     interleaves the recipe's planes, and the PNG / TIFF bytes are encoded on
-    the device; the host writes finished files.  Same files, names and order
-    as the reference; ``workers`` is accepted for signature compatibility."""
-    from .image_io import save_image
+    the device; the host writes finished files -- a few encodes stay in flight
+    and a small thread pool writes finished files while the next planes encode.
+    Same files, names and order as the reference; ``workers`` is accepted for
+    signature compatibility."""
+    from collections import deque
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .image_io import save_image, save_image_start
     from .projection import project_stack
 
     if fmt not in ("png", "tif"):
@@ -461,21 +468,30 @@ def render_planes(stack, model: ProjectionModel, specs: list[RenderSpec], out_di
     needed = set() if recipe is None else {recipe.red, recipe.green, recipe.blue}
     recipe_planes: dict = {}
     step = _render_batch(ds, len(specs))
-    for i in range(0, len(components), step):
-        batch = components[i:i + step]
-        planes = project_stack(ds, model, components=batch, workers=workers)
-        ranges = planes[0].minmax.cpu().numpy()   # [-min_0.., max_0..] of the batch
-        nb = len(batch)
-        for j, (k, plane) in enumerate(zip(batch, planes)):
-            for s_i, spec in enumerate(specs):
-                if spec.mode == "full" and -ranges[j] == ranges[nb + j]:
-                    _zeros_warning("constant score plane")   # rendering.py:128-129
-                img = rescale(plane, spec, model=model, k=k)
-                path = out_dir / plane_filename(run_name, k, spec, fmt)
-                save_image(img, path, compression=compression)
-                result.plane_paths.append(path)
-                if s_i == 0 and k in needed:
-                    recipe_planes[k] = img
+    inflight: deque = deque()     # encodes enqueued on the device, oldest first
+    writes = []
+    with ThreadPoolExecutor(max_workers=_WRITERS) as pool:
+        for i in range(0, len(components), step):
+            batch = components[i:i + step]
+            planes = project_stack(ds, model, components=batch, workers=workers)
+            ranges = planes[0].minmax.cpu().numpy()   # [-min_0.., max_0..] of the batch
+            nb = len(batch)
+            for j, (k, plane) in enumerate(zip(batch, planes)):
+                for s_i, spec in enumerate(specs):
+                    if spec.mode == "full" and -ranges[j] == ranges[nb + j]:
+                        _zeros_warning("constant score plane")   # rendering.py:128-129
+                    img = rescale(plane, spec, model=model, k=k)
+                    path = out_dir / plane_filename(run_name, k, spec, fmt)
+                    inflight.append(save_image_start(img, path, compression=compression))
+                    if len(inflight) > _ENCODES_IN_FLIGHT:
+                        writes.append(pool.submit(inflight.popleft()))
+                    result.plane_paths.append(path)
+                    if s_i == 0 and k in needed:
+                        recipe_planes[k] = img
+        while inflight:
+            writes.append(pool.submit(inflight.popleft()))
+        for w in writes:
+            w.result()            # re-raises a writer's DataError
     if recipe is not None:
         missing = sorted(needed - set(recipe_planes))
         if missing:
