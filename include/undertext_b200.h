@@ -294,6 +294,11 @@ int ut_encode_tiff(const void* img, int64_t rows, int64_t cols, int32_t channels
 int ut_decode_strips(const uint8_t* src, const int64_t* in_off, const int64_t* in_len, int64_t nstrips,
                      int32_t compression, uint8_t* dst, const int64_t* out_off, const int64_t* out_len,
                      int32_t* status, void* stream);
+/* ut_decode_streams: the same with a promise about the largest out_len of the batch
+ * (0 = unknown); deflate streams of <= 8 KB each take a small-window kernel. */
+int ut_decode_streams(const uint8_t* src, const int64_t* in_off, const int64_t* in_len, int64_t nstreams,
+                      int32_t compression, uint8_t* dst, const int64_t* out_off, const int64_t* out_len,
+                      int64_t max_out_len, int32_t* status, void* stream);
 int ut_unpredict(void* img, int32_t depth, int64_t rows, int64_t cols, int32_t channels,
                  int32_t predictor, int32_t swap_bytes, void* stream);
 int ut_untile(const uint8_t* tiles, uint8_t* img, int64_t rows, int64_t row_bytes, int64_t tile_rows,

@@ -32,7 +32,7 @@ EXPORTS = (
     "ut_stretch", "ut_plane_minmax_ws", "ut_plane_minmax", "ut_linear_to_codes",
     "ut_plane_select_ws", "ut_plane_select", "ut_normalize_ws", "ut_normalize_stack",
     "ut_synth_cube", "ut_class_of", "ut_encode_ws", "ut_encode_bound", "ut_encode_png",
-    "ut_encode_tiff", "ut_compose_rgb", "ut_decode_strips", "ut_unpredict", "ut_untile", "ut_png_unfilter",
+    "ut_encode_tiff", "ut_compose_rgb", "ut_decode_strips", "ut_decode_streams", "ut_unpredict", "ut_untile", "ut_png_unfilter",
     "ut_comm_available", "ut_comm_unique_id", "ut_comm_init", "ut_comm_destroy",
     "ut_allreduce_f64", "ut_allreduce_f32", "ut_allgather_f64",
 )
@@ -91,6 +91,7 @@ _SIGS = {
     "ut_class_of": (I32, [P, I32, P, I64, P, P]),
     "ut_compose_rgb": (I32, [P, P, P, I32, I64, P, P]),
     "ut_decode_strips": (I32, [P, P, P, I64, I32, P, P, P, P, P]),
+    "ut_decode_streams": (I32, [P, P, P, I64, I32, P, P, P, I64, P, P]),
     "ut_unpredict": (I32, [P, I32, I64, I64, I32, I32, I32, P]),
     "ut_untile": (I32, [P, P, I64, I64, I64, I64, I64, I64, P]),
     "ut_png_unfilter": (I32, [P, P, I64, P, P, P]),

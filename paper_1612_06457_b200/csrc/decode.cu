@@ -251,7 +251,8 @@ __device__ int inflate_one(const uint8_t* in, int64_t in_len, uint8_t* out, int6
 // memory window (the deflate history), Huffman codes of <= 9 bits resolve with
 // one shared-memory lookup, matches are copied by all lanes, and the window is
 // written to global memory in 8 KB pieces (with the Adler-32 sums) by all lanes.
-constexpr int kWinBits = 15, kWin = 1 << kWinBits, kWinMask = kWin - 1;
+constexpr int kWinBitsBig = 15;     // 32 KB window: the deflate history
+constexpr int kWinBitsSmall = 13;   // 8 KB: streams that inflate to <= 8 KB (one-row strips) -- 2.4x the warps per SM
 constexpr int kFlush = 8192;
 constexpr int kLitBits = 11, kDistBits = 8;   // index bits of the litlen / distance lookup tables
 
@@ -364,7 +365,9 @@ __device__ void wi_build_lit2(const uint16_t* fast, uint32_t* lit2, int lane) {
   __syncwarp();
 }
 
+template <int WB>
 struct WarpSmem {
+  static constexpr int kWin = 1 << WB, kWinMask = kWin - 1;
   uint8_t win[kWin];
   uint16_t litfast[1 << kLitBits];
   uint16_t distfast[1 << kDistBits];
@@ -374,6 +377,7 @@ struct WarpSmem {
 };
 
 // Adler-32 of win[from, from + n) folded into (a, b); all lanes, n <= kFlush
+template <int kWinMask>
 __device__ __forceinline__ void wi_flush(const uint8_t* win, uint8_t* out, int64_t from, int n,
                                          uint32_t& a, uint32_t& b, int lane) {
   unsigned long long sa = 0, sb = 0;
@@ -391,8 +395,11 @@ __device__ __forceinline__ void wi_flush(const uint8_t* win, uint8_t* out, int64
   a = (uint32_t)((a + sa) % 65521ull);
 }
 
+template <int WB>
 __device__ int inflate_warp(const uint8_t* in, int64_t in_len, uint8_t* out, int64_t out_len,
-                            WarpSmem& m, int lane) {
+                            WarpSmem<WB>& m, int lane) {
+  constexpr int kWinMask = WarpSmem<WB>::kWinMask;
+  if (WB < kWinBitsBig && out_len > WarpSmem<WB>::kWin) return kLong;   // caller's promise broken
   if (in_len < 2) return kHeader;
   const uint32_t cmf = in[0], flg = in[1];
   if ((cmf & 15) != 8 || (cmf >> 4) > 7 || ((cmf << 8) | flg) % 31 != 0 || (flg & 0x20)) return kHeader;
@@ -435,7 +442,7 @@ __device__ int inflate_warp(const uint8_t* in, int64_t in_len, uint8_t* out, int
         if (lane == 0) m.win[(o + k) & kWinMask] = (uint8_t)v;
         if (((o + k + 1) & (kFlush - 1)) == 0) {
           __syncwarp();
-          wi_flush(m.win, out, flushed, kFlush, a, b, lane);
+          wi_flush<kWinMask>(m.win, out, flushed, kFlush, a, b, lane);
           flushed += kFlush;
         }
       }
@@ -595,7 +602,7 @@ __device__ int inflate_warp(const uint8_t* in, int64_t in_len, uint8_t* out, int
       }
       if (o - flushed >= kFlush) {
         __syncwarp();
-        wi_flush(m.win, out, flushed, kFlush, a, b, lane);
+        wi_flush<kWinMask>(m.win, out, flushed, kFlush, a, b, lane);
         flushed += kFlush;
         __syncwarp();
       }
@@ -606,7 +613,7 @@ __device__ int inflate_warp(const uint8_t* in, int64_t in_len, uint8_t* out, int
   __syncwarp();
   while (flushed < o) {
     const int n = (int)((o - flushed) < kFlush ? (o - flushed) : kFlush);
-    wi_flush(m.win, out, flushed, n, a, b, lane);
+    wi_flush<kWinMask>(m.win, out, flushed, n, a, b, lane);
     flushed += n;
   }
   // Adler-32 trailer (big-endian) after the last block, byte aligned
@@ -619,11 +626,12 @@ __device__ int inflate_warp(const uint8_t* in, int64_t in_len, uint8_t* out, int
   return ((b << 16) | a) == want ? 0 : kAdler;
 }
 
+template <int WB>
 __global__ void __launch_bounds__(32) inflate_warp_kernel(const uint8_t* __restrict__ src, const int64_t* in_off,
                                                           const int64_t* in_len, uint8_t* dst,
                                                           const int64_t* out_off, const int64_t* out_len,
                                                           int32_t* status) {
-  __shared__ __align__(16) WarpSmem m;   // 38.6 KB, static: table and window addresses are compile-time offsets
+  __shared__ __align__(16) WarpSmem<WB> m;   // static (46.6 / 22 KB): table and window addresses are compile-time offsets
   const int64_t i = blockIdx.x;
   const int rc = inflate_warp(src + in_off[i], in_len[i], dst + out_off[i], out_len[i], m, (int)threadIdx.x);
   if (threadIdx.x == 0) status[i] = rc;
@@ -911,18 +919,35 @@ __global__ void __launch_bounds__(256) png_rows_kernel(const uint8_t* __restrict
   }
 }
 
+// One warp per row: a chunk of the row per step (32 samples, or 30 for RGB so that
+// a chunk holds whole pixels), the running sums of Predictor 2 by a shuffle scan
+// along each channel's chain (offsets ch, 2 ch, 4 ch, ...) plus the carry of the
+// previous chunk -- coalesced accesses and 32x the threads of a thread per row.
 template <typename T>
-__global__ void unpredict_kernel(T* img, int64_t rows, int64_t spr, int ch, int predictor, int swap) {
-  const int64_t y = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (y >= rows) return;
+__global__ void __launch_bounds__(128) unpredict_kernel(T* img, int64_t rows, int64_t spr, int ch,
+                                                        int predictor, int swap) {
+  const int lane = threadIdx.x & 31;
+  const int64_t y = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (y >= rows) return;   // warp-uniform
   T* row = img + y * spr;
-  if (swap && sizeof(T) == 2)
-    for (int64_t x = 0; x < spr; ++x) {
-      const uint16_t v = (uint16_t)row[x];
-      row[x] = (T)((v >> 8) | (v << 8));
+  const int chunk = 32 - (32 % ch);
+  const int tail = chunk - ch + lane % ch;   // lane holding this lane's channel at the chunk's end
+  uint32_t carry = 0u;
+  for (int64_t x0 = 0; x0 < spr; x0 += chunk) {
+    const int64_t x = x0 + lane;
+    const bool active = lane < chunk && x < spr;
+    uint32_t v = active ? (uint32_t)row[x] : 0u;
+    if (swap && sizeof(T) == 2) v = ((v >> 8) | (v << 8)) & 0xffffu;
+    if (predictor == 2) {
+      for (int o = ch; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+      }
+      v += carry;
+      carry = __shfl_sync(0xffffffffu, v, tail);
     }
-  if (predictor == 2)
-    for (int64_t x = ch; x < spr; ++x) row[x] = (T)(row[x] + row[x - ch]);
+    if (active) row[x] = (T)v;
+  }
 }
 
 }  // namespace
@@ -935,6 +960,13 @@ extern "C" {
 int ut_decode_strips(const uint8_t* src, const int64_t* in_off, const int64_t* in_len, int64_t nstrips,
                      int32_t compression, uint8_t* dst, const int64_t* out_off, const int64_t* out_len,
                      int32_t* status, void* stream) {
+  return ut_decode_streams(src, in_off, in_len, nstrips, compression, dst, out_off, out_len, 0, status,
+                           stream);
+}
+
+int ut_decode_streams(const uint8_t* src, const int64_t* in_off, const int64_t* in_len, int64_t nstrips,
+                      int32_t compression, uint8_t* dst, const int64_t* out_off, const int64_t* out_len,
+                      int64_t max_out_len, int32_t* status, void* stream) {
   UT_REQUIRE(nstrips >= 0, "negative strip count");
   UT_REQUIRE(compression == 1 || compression == 8 || compression == 5,
              "strip compression must be 1 (none), 5 (LZW) or 8 (zlib deflate), got %d", compression);
@@ -967,8 +999,16 @@ int ut_decode_strips(const uint8_t* src, const int64_t* in_off, const int64_t* i
           src, in_off, in_len, nstrips, dst, out_off, out_len, status);
       UT_CHECK_LAUNCH("inflate_kernel");
     } else {
-      static_assert(sizeof(WarpSmem) <= 48 * 1024, "inflate window + tables must fit static shared memory");
-      inflate_warp_kernel<<<(unsigned)nstrips, 32, 0, st>>>(src, in_off, in_len, dst, out_off, out_len, status);
+      static_assert(sizeof(WarpSmem<kWinBitsBig>) <= 48 * 1024,
+                    "inflate window + tables must fit static shared memory");
+      // streams known to inflate to <= 8 KB each (e.g. one-row strips) take the
+      // small-window kernel: 22 KB of shared memory per warp instead of 46.6 KB
+      if (max_out_len > 0 && max_out_len <= (1 << kWinBitsSmall))
+        inflate_warp_kernel<kWinBitsSmall><<<(unsigned)nstrips, 32, 0, st>>>(src, in_off, in_len, dst, out_off,
+                                                                             out_len, status);
+      else
+        inflate_warp_kernel<kWinBitsBig><<<(unsigned)nstrips, 32, 0, st>>>(src, in_off, in_len, dst, out_off,
+                                                                           out_len, status);
       UT_CHECK_LAUNCH("inflate_warp_kernel");
     }
   }
@@ -982,7 +1022,8 @@ int ut_unpredict(void* img, int32_t depth, int64_t rows, int64_t cols, int32_t c
   UT_REQUIRE(rows >= 0 && cols >= 0 && channels >= 1, "bad image geometry");
   if (rows == 0 || cols == 0 || (predictor == 1 && !(swap_bytes && depth == 16))) return UT_OK;
   cudaStream_t st = as_stream(stream);
-  const unsigned grid = (unsigned)((rows + 127) / 128);
+  UT_REQUIRE(channels <= 16, "ut_unpredict: at most 16 channels");
+  const unsigned grid = (unsigned)((rows * 32 + 127) / 128);   // one warp per row
   if (depth == 8)
     unpredict_kernel<uint8_t><<<grid, 128, 0, st>>>(static_cast<uint8_t*>(img), rows, cols * channels,
                                                     channels, predictor, 0);

@@ -402,6 +402,22 @@ def _png_plan(data: bytes) -> dict:
             "out_len": np.asarray([h * (rb + 1)], dtype=np.int64)}
 
 
+_STAGING: dict = {}
+
+
+def _pinned_staging(nbytes: int) -> torch.Tensor:
+    """A cached, grow-only pinned host buffer for the compressed bytes (pinning
+    memory costs more than decoding a small stack; the buffer is reused once the
+    previous copy out of it has completed)."""
+    buf, busy = _STAGING.get("buf"), _STAGING.get("busy")
+    if busy is not None:
+        busy.synchronize()            # the last H2D out of the buffer
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        _STAGING["buf"] = buf
+    return buf[:nbytes]
+
+
 def _plan(data: bytes) -> dict:
     if data[:8] == _PNG_SIGNATURE:
         return _png_plan(data)
@@ -419,11 +435,13 @@ def decode_batch(datas: list, device=None) -> list:
     file_base = np.cumsum([0] + [_align(len(pl["payload"]), 16) for pl in plans])
     out_base = np.cumsum([0] + [pl["region"] for pl in plans])
     with torch.cuda.device(device):
-        host = torch.empty(int(file_base[-1]) + 16, dtype=torch.uint8, pin_memory=True)
+        host = _pinned_staging(int(file_base[-1]) + 16)
         hv = host.numpy()
         for pl, b0 in zip(plans, file_base):
             hv[b0:b0 + len(pl["payload"])] = np.frombuffer(pl["payload"], dtype=np.uint8)
         src = host.to(device, non_blocking=True)
+        _STAGING["busy"] = torch.cuda.Event()
+        _STAGING["busy"].record()
         out = torch.empty(int(out_base[-1]) + 16, dtype=torch.uint8, device=device)
         L = _lib.lib()
         s = dev.stream_handle()
@@ -439,10 +457,11 @@ def decode_batch(datas: list, device=None) -> list:
                                                 cat("out_len", None)])).to(device)
             n = tables.shape[1]
             status = torch.empty(n, dtype=torch.int32, device=device)
-            _lib.check(L.ut_decode_strips(src.data_ptr(), tables[0].data_ptr(),
-                                          tables[1].data_ptr(), n, code, out.data_ptr(),
-                                          tables[2].data_ptr(), tables[3].data_ptr(),
-                                          status.data_ptr(), s), "ut_decode_strips")
+            largest = int(max(int(plans[i]["out_len"].max()) for i in sel))
+            _lib.check(L.ut_decode_streams(src.data_ptr(), tables[0].data_ptr(),
+                                           tables[1].data_ptr(), n, code, out.data_ptr(),
+                                           tables[2].data_ptr(), tables[3].data_ptr(), largest,
+                                           status.data_ptr(), s), "ut_decode_streams")
             statuses.append(status)
         pngs = [i for i, pl in enumerate(plans) if pl["kind"] == "png"]
         if pngs:
