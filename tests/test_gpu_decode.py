@@ -379,10 +379,9 @@ class TestLoadStack:
 
 
 def test_measured_path_never_uses_host_codecs(monkeypatch):
-    """The measured path
-    -- the cube resident in HBM, fit, projection, stretch, as bench.py times it
-    (CVA, the PCA companion and the streamed folio batch) -- must never reach a
-    host codec: every cv2 entry point is made to fail here."""
+    """The measured path -- the cube resident in HBM, fit, projection, stretch, as
+    bench.py times it (CVA, the PCA companion and the streamed folio batch) -- must
+    never reach a host codec: every cv2 entry point is made to fail here."""
     from dataclasses import replace
 
     import cv2
