@@ -15,6 +15,7 @@ byte-deterministic.
 from __future__ import annotations
 
 import struct
+import threading
 import zlib
 from pathlib import Path
 
@@ -403,6 +404,7 @@ def _png_plan(data: bytes) -> dict:
 
 
 _STAGING: dict = {}
+_STAGING_LOCK = threading.Lock()   # one decode fills / copies out of the staging buffer at a time
 
 
 def _pinned_staging(nbytes: int) -> torch.Tensor:
@@ -435,13 +437,14 @@ def decode_batch(datas: list, device=None) -> list:
     file_base = np.cumsum([0] + [_align(len(pl["payload"]), 16) for pl in plans])
     out_base = np.cumsum([0] + [pl["region"] for pl in plans])
     with torch.cuda.device(device):
-        host = _pinned_staging(int(file_base[-1]) + 16)
-        hv = host.numpy()
-        for pl, b0 in zip(plans, file_base):
-            hv[b0:b0 + len(pl["payload"])] = np.frombuffer(pl["payload"], dtype=np.uint8)
-        src = host.to(device, non_blocking=True)
-        _STAGING["busy"] = torch.cuda.Event()
-        _STAGING["busy"].record()
+        with _STAGING_LOCK:
+            host = _pinned_staging(int(file_base[-1]) + 16)
+            hv = host.numpy()
+            for pl, b0 in zip(plans, file_base):
+                hv[b0:b0 + len(pl["payload"])] = np.frombuffer(pl["payload"], dtype=np.uint8)
+            src = host.to(device, non_blocking=True)
+            _STAGING["busy"] = torch.cuda.Event()
+            _STAGING["busy"].record()
         out = torch.empty(int(out_base[-1]) + 16, dtype=torch.uint8, device=device)
         L = _lib.lib()
         s = dev.stream_handle()
