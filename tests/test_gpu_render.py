@@ -68,6 +68,34 @@ def test_render_planes_files(tmp_path, case, fmt, compression):
     assert np.array_equal(comp, want)
 
 
+def test_render_planes_write_failure_is_a_data_error(tmp_path, case):
+    """A file that cannot be written surfaces as the reference's DataError even
+    though the writes run on the writer pool, and the other planes are written."""
+    cube, stack, model = case
+    (tmp_path / "run_plane01_full.png").mkdir()        # a directory where plane 1 should go
+    with pytest.raises(ut.DataError, match="failed to write image"):
+        ut.render_planes(stack, model, [ut.RenderSpec()], tmp_path)
+    assert (tmp_path / "run_plane00_full.png").is_file()
+
+
+def test_pending_encodes_finish_in_any_order(case):
+    """encode_*_start keeps encodes in flight; their bytes do not depend on when or
+    where (another thread) they are collected."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_1612_06457_b200 import image_io
+
+    cube, stack, model = case
+    planes = ut.project_stack(ut.stack.on_device(stack), model)
+    imgs = [ut.rescale_full(p) for p in planes]
+    want = [image_io.encode_png(i) for i in imgs] + [image_io.encode_tiff(i, "deflate") for i in imgs]
+    pend = [image_io.encode_png_start(i) for i in imgs] + \
+           [image_io.encode_tiff_start(i, "deflate") for i in imgs]
+    with ThreadPoolExecutor(max_workers=3) as pool:
+        got = list(pool.map(lambda q: q.bytes(), reversed(pend)))[::-1]
+    assert got == want
+
+
 def test_render_planes_device_stack_and_subset(tmp_path, case):
     cube, stack, model = case
     ds = ut.stack.on_device(stack)
