@@ -1054,7 +1054,13 @@ int launch_region_dmma(const Region& r, RegionWs ws, double* moments, cudaStream
   rp.npix = r.npix;
   rp.bands = r.bands;
   const int64_t ntiles = (r.npix + kRdP - 1) / kRdP;
-  const int64_t g = 148;  // fixed (not the device's SM count): results independent of the GPU
+  // fixed by the band count (not the device's SM count): results independent of the
+  // GPU.  Up to 16 bands two CTAs fit an SM (3 stages x 16 bands x 2 KB = 99 KB each):
+  // twice the warps hide the LDS -> F2F -> DMMA latency (cfg 2: K2' 114 -> see DESIGN)
+#ifndef UT_RD_G2
+#define UT_RD_G2 1
+#endif
+  const int64_t g = (UT_RD_G2 && rd_smem<T>(r.bands) <= 100 * 1024) ? 296 : 148;
   rp.G = (int)(ntiles < g ? ntiles : g);
   rp.shift = ws.shift;
   rp.part = ws.part;
