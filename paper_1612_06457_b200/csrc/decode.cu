@@ -318,7 +318,7 @@ __device__ __forceinline__ int wi_slow_sym(WarpIn& s, const Huff* h) {
 }
 template <int BITS>
 __device__ __forceinline__ int wi_sym(WarpIn& s, const Huff* h, const uint16_t* fast) {
-  wi_refill(s);   // >= 33 bits: enough for a code (15) and its extra bits (13)
+  wi_refill(s);   // >= 32 bits: enough for a code (15) and its extra bits (13)
   const uint32_t e = fast[s.buf & ((1u << BITS) - 1)];
   if (e & 15u) {
     s.buf >>= (e & 15u);
@@ -526,8 +526,8 @@ __device__ int inflate_warp(const uint8_t* in, int64_t in_len, uint8_t* out, int
         // (32-bit counters; every lane stores the same byte, so nothing diverges).
         // ncu of a PNG stream: the loop is bound by its taken branches and by the
         // shared-window base ptxas rebuilds (S2UR -> ULEA) in front of every lookup,
-        // so three literals are decoded per refill check -- after a refill the
-        // buffer holds >= 33 bits = three table codes of <= 11 bits -- and the table
+        // so three lookups are decoded per refill check -- topped up to >= 33 bits =
+        // three table codes of <= 11 bits -- and the table
         // / window addresses live in registers the compiler cannot see through.
         const int64_t stop = flushed + kFlush < out_len ? flushed + kFlush : out_len;
         uint32_t left = stop > o ? (uint32_t)(stop - o) : 0u;
@@ -561,6 +561,7 @@ __device__ int inflate_warp(const uint8_t* in, int64_t in_len, uint8_t* out, int
         };
         while (left >= 6u) {   // three lookups (<= 33 bits, <= 6 literals) per refill check
           wi_refill(s);
+          wi_refill(s);          // a refill of an empty buffer leaves 32 bits: top it up to >= 33
           if (!literal()) break;
           if (!literal()) break;
           if (!literal()) break;

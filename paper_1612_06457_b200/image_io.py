@@ -496,9 +496,11 @@ def decode_batch(datas: list, device=None) -> list:
                                           pl["predictor"], pl["swap"], s), "ut_unpredict")
             images.append(img.view(pl["h"], pl["w"], pl["ch"]) if pl["ch"] == 3
                           else img.view(pl["h"], pl["w"]))
-        bad = sum(int((st != 0).sum().item()) for st in statuses)
-    if bad:
-        raise DataError(f"image data has {bad} undecodable stream(s)")
+        codes = torch.cat([st[st != 0] for st in statuses]).cpu().tolist() if statuses else []
+    if codes:
+        names = {1: "malformed", 2: "too short", 3: "too long", 4: "checksum", 5: "header"}
+        kinds = sorted({names.get(int(c), str(c)) for c in codes})
+        raise DataError(f"image data has {len(codes)} undecodable stream(s) ({', '.join(kinds)})")
     return images
 
 

@@ -411,3 +411,46 @@ def test_measured_path_never_uses_host_codecs(monkeypatch):
     fs.run()
     torch.cuda.synchronize()
     fs.check()
+
+
+def test_decoders_fuzz_vs_cv2():
+    """Seeded random images (noise, flat, smooth, periodic rows; gray / RGB, 8 / 16 bit)
+    through every container cv2 writes and the device reads; iterations 22, 26 and 44
+    of this sequence are streams whose literal runs empty the inflate's bit buffer
+    exactly (a refill then holds 32 bits, one short of three 11-bit codes) -- the
+    case a first version of the warp decoder got wrong."""
+    rng = np.random.default_rng(12345)
+    checked = 0
+    for it in range(60):
+        h, w = int(rng.integers(1, 300)), int(rng.integers(1, 700))
+        ch = int(rng.choice([1, 3]))
+        dt = rng.choice([np.uint8, np.uint16])
+        top = np.iinfo(dt).max
+        kind = rng.integers(0, 4)
+        shape = (h, w) if ch == 1 else (h, w, 3)
+        if kind == 0:
+            img = rng.integers(0, top + 1, size=shape).astype(dt)
+        elif kind == 1:
+            img = np.full(shape, rng.integers(0, top + 1), dtype=dt)
+        elif kind == 2:
+            y, x = np.mgrid[0:h, 0:w]
+            base = (np.sin(x / 9.0) + np.cos(y / 7.0) + 2) / 4 * top
+            img = (base if ch == 1 else base[..., None] * np.array([1, .5, .25])).astype(dt)
+        else:
+            img = np.tile(rng.integers(0, top + 1, size=(1, int(rng.integers(1, 40))) + shape[2:]).astype(dt),
+                          (h, w // 1 + 1) + (1,) * (len(shape) - 2))[:, :w]
+            img = np.ascontiguousarray(img.reshape(shape))
+        payload = np.ascontiguousarray(img[:, :, ::-1]) if ch == 3 else img
+        for ext, params in ((".png", []), (".png", [cv2.IMWRITE_PNG_COMPRESSION, int(rng.integers(0, 10))]),
+                            (".tif", [cv2.IMWRITE_TIFF_COMPRESSION, 5]), (".tif", [cv2.IMWRITE_TIFF_COMPRESSION, 8]),
+                            (".tif", [cv2.IMWRITE_TIFF_COMPRESSION, 1])):
+            ok, buf = cv2.imencode(ext, payload, params)
+            assert ok
+            got = image_io.decode_batch([buf.tobytes()])[0].cpu().numpy()
+            assert got.dtype == img.dtype and np.array_equal(got, img), (it, ext, params, shape, kind)
+            checked += 1
+        t = torch.from_numpy(img).cuda()
+        for data in (image_io.encode_png(t), image_io.encode_tiff(t, "deflate")):
+            assert np.array_equal(image_io.decode_batch([data])[0].cpu().numpy(), img), (it, shape)
+            checked += 1
+    assert checked == 60 * 7
