@@ -33,7 +33,10 @@ inline int ensure_smem(SmemAttr& a, K kern, size_t bytes, const char* what) {
   size_t* slot = (dev >= 0 && dev < 64) ? &a.bytes[dev] : nullptr;
   if (slot && *slot >= bytes) return UT_OK;
   const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e != cudaSuccess) return cuda_status(e, what);
+  if (e != cudaSuccess) {
+    cudaGetLastError();   // do not leave it for the next launch check to report
+    return cuda_status(e, what);
+  }
   if (slot) *slot = bytes;
   return UT_OK;
 }

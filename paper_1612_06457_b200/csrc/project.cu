@@ -810,8 +810,11 @@ int launch_kg(ProjParams& p, bool vector_ok, cudaStream_t st) {
           (p.npix % 2) == 0)
         return launch_dmma<T, KG>(p, st);
       constexpr int VT = (16 / (int)sizeof(T)) < 2 ? 1 : ((8 / (int)sizeof(T)) < 2 ? 2 : 8 / (int)sizeof(T));
-      if ((p.npix % VT) == 0) return launch_tma<T, VT, KG, F64, 256>(p, st);
-    } else {
+      // (wide fp64 cubes: one 512-pixel stage of > 18 bands would not fit three times
+      // into shared memory -- those take the direct-load kernel below)
+      if ((p.npix % VT) == 0 && tma_shape<T, VT, 256>(p.bands).smem <= 227 * 1024)
+        return launch_tma<T, VT, KG, F64, 256>(p, st);
+    } else if (tma_shape<T, VEC, 128>(p.bands).smem <= 227 * 1024) {
       return launch_tma<T, VEC, KG, F64, 128>(p, st);
     }
   }

@@ -279,3 +279,68 @@ def test_bad_point_reported_in_caller_order():
     pipe.run()
     with pytest.raises(ut.DataError, match=r"\(51, 3\) outside"):
         pipe.check()
+
+
+@pytest.mark.parametrize("b,k", [(29, 2), (32, 3), (20, 1), (19, 2)])
+def test_wide_fp64_cube_few_components(b, k):
+    """fp64 cubes of more than 18 bands with fewer than 4 components: a 512-pixel
+    stage of the bulk-copy projector would not fit shared memory three times, so the
+    direct-load projector runs (the launch used to fail with an invalid shared-memory
+    attribute; found by fuzzing shapes against the oracle)."""
+    rng = np.random.default_rng(100 * b + k)
+    cube, cmap = cube_of(rng, b, 52, 160, np.float64, classes=4)
+    xs, ys, ls = pick_points(rng, cmap, 60)
+    pipe = ut.CvaPipeline(device_stack(cube), xs, ys, ls, k=k)
+    codes = pipe.run().cpu().numpy()
+    pipe.check()
+    m = pipe.model()
+    want = oracle.project(cube, {"mean": m.mean, "std": None, "coefficients": m.coefficients})
+    assert plane_close(pipe.scores.double().cpu().numpy(), want) <= 1e-6
+    for j in range(k):
+        assert np.array_equal(codes[j], oracle.rescale_full(pipe.scores[j].double().cpu().numpy()))
+
+
+def test_path_fuzz_vs_oracle():
+    """Seeded random shapes / dtypes / class counts / point orders through the whole
+    path (fit, planes, codes, PCA) against the oracle."""
+    rng = np.random.default_rng(2024)
+    done = 0
+    for it in range(40):
+        b, classes = int(rng.integers(1, 33)), int(rng.integers(2, 9))
+        h, w = int(rng.integers(8, 200)), int(rng.integers(8, 400))
+        dtype = DTYPES[int(rng.integers(0, len(DTYPES)))]
+        cube, cmap = cube_of(rng, b, h, w, dtype, classes=classes)
+        per = int(rng.integers(max(3, b // classes + 2), 120))
+        xs, ys, ls = pick_points(rng, cmap, per)
+        if len(np.unique(ls)) < 2:
+            continue
+        if it % 2:
+            perm = rng.permutation(len(ls))
+            xs, ys, ls = xs[perm], ys[perm], ls[perm]
+        k = int(rng.integers(1, min(b, len(np.unique(ls)) - 1) + 1))
+        ds = device_stack(cube)
+        pipe = ut.CvaPipeline(ds, xs, ys, ls, k=k)
+        codes = pipe.run().cpu().numpy()
+        hst = pipe.check()
+        ref = oracle.fit_cva(oracle.assemble(cube, xs, ys), ls, k=k)
+        sp = ref["scatter"]
+        case = (it, b, classes, h, w, dtype.__name__, k)
+        assert np.array_equal(hst["counts"].astype(int), sp["counts"]), case
+        assert rel_close(hst["within"], sp["within"], 1e-9), case
+        assert rel_close(hst["between"], sp["between"], 1e-9), case
+        lam = np.asarray(ref["eigenvalues"])
+        sig = lam > 1e-6 * lam.max()
+        assert np.all(np.abs(hst["evals"][:k][sig] - lam[sig]) <= 1e-9 * np.abs(lam[sig])), case
+        m = pipe.model()
+        want = oracle.project(cube, {"mean": m.mean, "std": None, "coefficients": m.coefficients})
+        assert plane_close(pipe.scores.double().cpu().numpy(), want) <= 1e-6, case
+        for j in range(k):
+            assert np.array_equal(codes[j],
+                                  oracle.rescale_full(pipe.scores[j].double().cpu().numpy())), case
+        pm = ut.fit_pca_unsupervised(ds, k=min(3, b))
+        rp = oracle.fit_pca_unsupervised(cube, k=min(3, b))
+        assert rel_close(pm.mean, rp["mean"], 1e-9), case
+        le = np.asarray(rp["eigenvalues"])
+        assert np.all(np.abs(np.asarray(pm.eigenvalues) - le) <= 1e-9 * (le.max() + np.abs(le))), case
+        done += 1
+    assert done >= 35
