@@ -331,7 +331,7 @@ def _tiff_plan(data: bytes) -> dict:
         if len(offs) != n or len(counts) != n:
             raise DataError(f"TIFF lists {len(offs)} tiles, expected {n}")
         tile_bytes = th * tw * px
-        if n * tile_bytes > 4 * (h * rb + tile_bytes):
+        if tile_bytes > max(1 << 26, 16 * h * rb):   # a 64 MB tile for a small image: refuse the scratch
             raise DataError("TIFF tile size does not fit the image")
         scratch0 = _align(h * rb)
         plan.update(tile_w=tw, tile_h=th, across=across, ntiles=n, scratch=scratch0,
