@@ -252,6 +252,12 @@ _TIFF_TYPES = {1: ("B", 1), 3: ("H", 2), 4: ("I", 4), 16: ("Q", 8)}
 _TIFF_CODES = {1: 1, 5: 5, 8: 8, 32946: 8}      # Compression tag -> decoder (raw, LZW, zlib)
 
 
+# the most a stream can expand: raw 1:1, deflate 1032:1 (RFC 1951: 258 bytes per 2 bits),
+# TIFF LZW 12-bit codes of strings up to a strip long (bounded here by 4096:1)
+_MAX_EXPANSION = {1: 1, 8: 1032, 5: 4096}
+_MAX_IMAGE_BYTES = 1 << 35
+
+
 class _Unsupported(Exception):
     """A file layout the device decoders do not handle (the caller uses cv2)."""
 
@@ -268,7 +274,11 @@ def _tiff_layout(data: bytes) -> dict:
     magic, ifd = struct.unpack(bo + "HI", data[2:8])
     if magic != 42:
         raise _Unsupported("not a classic TIFF")
+    if ifd + 2 > len(data):
+        raise DataError("TIFF directory runs past the end of the file")
     (n,) = struct.unpack(bo + "H", data[ifd:ifd + 2])
+    if ifd + 2 + 12 * n > len(data):
+        raise DataError("TIFF directory runs past the end of the file")
     tags = {}
     for i in range(n):
         tag, typ, count = struct.unpack(bo + "HHI", data[ifd + 2 + 12 * i:ifd + 10 + 12 * i])
@@ -278,8 +288,10 @@ def _tiff_layout(data: bytes) -> dict:
         raw_at = ifd + 10 + 12 * i
         if size * count > 4:
             (raw_at,) = struct.unpack(bo + "I", data[raw_at:raw_at + 4])
+        if raw_at + size * count > len(data):
+            raise DataError(f"TIFF tag {tag} runs past the end of the file")
         tags[tag] = list(struct.unpack(bo + code * count, data[raw_at:raw_at + size * count]))
-    get = lambda t, d=None: tags.get(t, [d])  # noqa: E731
+    get = lambda t, d=None: tags.get(t) or [d]  # noqa: E731
     lay = {
         "bo": bo, "width": get(256)[0], "height": get(257)[0], "bps": get(258, 1),
         "compression": get(259, 1)[0], "photometric": get(262, 1)[0], "spp": get(277, 1)[0],
@@ -316,6 +328,8 @@ def _tiff_plan(data: bytes) -> dict:
     depth = int(lay["bps"][0])
     px = ch * depth // 8
     rb = w * px
+    if h * rb > _MAX_IMAGE_BYTES:
+        raise DataError(f"image of {h * rb} bytes is larger than the decoder accepts")
     plan = {"kind": "tiff", "payload": data, "h": h, "w": w, "ch": ch, "depth": depth,
             "bytes": h * rb, "code": _TIFF_CODES[lay["compression"]],
             "predictor": int(lay["predictor"]), "swap": int(lay["bo"] == ">" and depth == 16),
@@ -421,9 +435,15 @@ def _pinned_staging(nbytes: int) -> torch.Tensor:
 
 
 def _plan(data: bytes) -> dict:
-    if data[:8] == _PNG_SIGNATURE:
-        return _png_plan(data)
-    return _tiff_plan(data)
+    plan = _png_plan(data) if data[:8] == _PNG_SIGNATURE else _tiff_plan(data)
+    if plan["bytes"] > _MAX_IMAGE_BYTES:
+        raise DataError(f"image of {plan['bytes']} bytes is larger than the decoder accepts")
+    limit = plan["counts"] * _MAX_EXPANSION[plan["code"]] + 64
+    if plan["code"] == 1 and plan["kind"] == "tiff":
+        limit = plan["counts"]
+    if np.any(plan["out_len"] > limit):
+        raise DataError("image data is too short for the image size in its header")
+    return plan
 
 
 def decode_batch(datas: list, device=None) -> list:
@@ -466,6 +486,7 @@ def decode_batch(datas: list, device=None) -> list:
                                            tables[2].data_ptr(), tables[3].data_ptr(), largest,
                                            status.data_ptr(), s), "ut_decode_streams")
             statuses.append(status)
+        _raise_on_bad_streams(statuses)   # before the filters / predictors run over damaged rows
         pngs = [i for i, pl in enumerate(plans) if pl["kind"] == "png"]
         if pngs:
             table = torch.from_numpy(np.asarray(
@@ -496,12 +517,16 @@ def decode_batch(datas: list, device=None) -> list:
                                           pl["predictor"], pl["swap"], s), "ut_unpredict")
             images.append(img.view(pl["h"], pl["w"], pl["ch"]) if pl["ch"] == 3
                           else img.view(pl["h"], pl["w"]))
-        codes = torch.cat([st[st != 0] for st in statuses]).cpu().tolist() if statuses else []
+        _raise_on_bad_streams(statuses[-1:] if pngs else [])
+    return images
+
+
+def _raise_on_bad_streams(statuses: list) -> None:
+    codes = torch.cat([st[st != 0] for st in statuses]).cpu().tolist() if statuses else []
     if codes:
         names = {1: "malformed", 2: "too short", 3: "too long", 4: "checksum", 5: "header"}
         kinds = sorted({names.get(int(c), str(c)) for c in codes})
         raise DataError(f"image data has {len(codes)} undecodable stream(s) ({', '.join(kinds)})")
-    return images
 
 
 def decode_tiff_batch(datas: list, device=None) -> list:

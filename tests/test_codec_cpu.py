@@ -202,3 +202,23 @@ def test_tiff_plan_tiles_and_lzw():
     jpeg = [e if e[0] != 259 else (259, 3, [7]) for e in strips]
     with pytest.raises(image_io._Unsupported):
         image_io._tiff_plan(_ifd_tiff(jpeg, bytes(300)))
+
+
+def test_damaged_tiff_headers_are_data_errors():
+    """Truncated files, directories / tag arrays past the end of the file, empty tag
+    arrays and sizes the data cannot fill are DataErrors on the host, before any
+    device work (found by tools/fuzz/fuzz_corrupt.py: they used to be struct.error)."""
+    img = np.arange(40 * 30, dtype=np.uint16).reshape(40, 30)
+    data = image_io._tiff_file(img.tobytes(), np.array([img.nbytes]), 40, 30, 1, 16, 1, 40)
+    assert image_io._tiff_plan(data)["bytes"] == img.nbytes
+    for cut in (9, len(data) - 5, len(data) - 60):
+        with pytest.raises(DataError):
+            image_io._plan(data[:cut])
+    far = bytearray(data)
+    far[4:8] = struct.pack("<I", len(data) + 100)          # directory offset past the end
+    with pytest.raises(DataError, match="directory"):
+        image_io._plan(bytes(far))
+    big = _ifd_tiff([(256, 4, [30]), (257, 4, [1 << 20]), (258, 3, [16]), (259, 3, [8]), (262, 3, [1]),
+                     (277, 3, [1]), (273, 4, [8]), (278, 4, [1 << 20]), (279, 4, [100])], bytes(100))
+    with pytest.raises(DataError, match="too short"):      # 100 bytes cannot inflate to 60 MB
+        image_io._plan(big)
