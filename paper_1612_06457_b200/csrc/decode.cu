@@ -978,16 +978,24 @@ int ut_decode_streams(const uint8_t* src, const int64_t* in_off, const int64_t* 
     strips_copy_kernel<<<(unsigned)nstrips, 256, 0, st>>>(src, in_off, in_len, dst, out_off, out_len, status);
     UT_CHECK_LAUNCH("strips_copy_kernel");
   } else if (compression == 5) {
-    // string tables: 6 bytes per code and stream, stream-ordered scratch
+    // string tables: 6 bytes per code and stream in a stream-ordered scratch buffer;
+    // at most 32768 streams (768 MB of tables) per launch, so a stack of many one-row
+    // strips does not ask for tens of gigabytes
+    constexpr int64_t kWave = 32768;
+    const int64_t wave = nstrips < kWave ? nstrips : kWave;
     void* tab = nullptr;
     const size_t per = 4096 * (sizeof(int32_t) + sizeof(uint16_t));
-    cudaError_t e = cudaMallocAsync(&tab, per * (size_t)nstrips, st);
+    cudaError_t e = cudaMallocAsync(&tab, per * (size_t)wave, st);
     if (e != cudaSuccess) return cuda_status(e, "ut_decode_strips: LZW tables");
     int32_t* pos = static_cast<int32_t*>(tab);
-    uint16_t* len = reinterpret_cast<uint16_t*>(pos + (size_t)nstrips * 4096);
-    lzw_kernel<<<(unsigned)((nstrips + kLzwThreads - 1) / kLzwThreads), kLzwThreads, 0, st>>>(
-        src, in_off, in_len, nstrips, dst, out_off, out_len, status, pos, len);
-    const cudaError_t le = cudaGetLastError();
+    uint16_t* len = reinterpret_cast<uint16_t*>(pos + (size_t)wave * 4096);
+    cudaError_t le = cudaSuccess;
+    for (int64_t s0 = 0; s0 < nstrips && le == cudaSuccess; s0 += wave) {
+      const int64_t n = nstrips - s0 < wave ? nstrips - s0 : wave;
+      lzw_kernel<<<(unsigned)((n + kLzwThreads - 1) / kLzwThreads), kLzwThreads, 0, st>>>(
+          src, in_off + s0, in_len + s0, n, dst, out_off + s0, out_len + s0, status + s0, pos, len);
+      le = cudaGetLastError();
+    }
     cudaFreeAsync(tab, st);
     if (le != cudaSuccess) return cuda_status(le, "lzw_kernel");
   } else {
